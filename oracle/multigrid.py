@@ -1,0 +1,88 @@
+"""Galerkin multigrid hierarchy, damped-Jacobi smoother and the V-cycle.
+
+Oracle (test infrastructure only).
+
+PAPER.md:1084-1111 (Sec. 6.1, "Multigrid idea"): ingredients (smoothers S_l, ~S_l with
+s_l, ~s_l steps; R_l, P_l; hierarchy A_l with A_0 := A), the V-cycle steps 1-3, and the
+Galerkin choice R_l := P_l^T, A_{l+1} := P_l^T A_l P_l.
+Readings:
+  R4  smoother = damped (weighted) Jacobi x <- x + omega_l D_l^{-1}(b - A_l x), the
+      data-parallel form north_star names in place of the paper's Gauss-Seidel;
+      omega_l = 4/(3 * 1.05 * rho_l), rho_l = generalized Rayleigh quotient
+      (v,A v)/(v,D v) after K=30 normalised power steps v <- D^{-1}A v / ||.||_2 from the
+      counter-based start vector inputs.hash_vector (same formula on both sides).
+  R5  coarsest level solved exactly (dense Cholesky, library primitive scipy cho_solve).
+  R6  levels: n_{l+1} = n_l/2 while n_l is even, the next interior size n_l/2+p-2 >= 1 and
+      d*(n_l+p-2)^d > 1500 (or exactly ``levels`` levels when requested).
+"""
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+from inputs import hash_vector
+from .transfer import prolongation
+
+NCOARSE_MAX = 1500
+POWER_STEPS = 30
+
+
+def level_sizes(d: int, p: int, n: int, levels: int = 0):
+    """Element counts n_0 > n_1 > ... > n_L of the hierarchy (reading R6)."""
+    ns = [n]
+    if levels > 0:
+        for _ in range(levels - 1):
+            if ns[-1] % 2 or ns[-1] // 2 + p - 2 < 1:
+                raise ValueError("hierarchy of %d levels impossible for n=%d, p=%d" % (levels, n, p))
+            ns.append(ns[-1] // 2)
+        return ns
+    while ns[-1] % 2 == 0 and ns[-1] // 2 + p - 2 >= 1 and d * (ns[-1] + p - 2) ** d > NCOARSE_MAX:
+        ns.append(ns[-1] // 2)
+    return ns
+
+
+def power_rho(A: sp.spmatrix, Ddiag: np.ndarray, steps: int = POWER_STEPS) -> float:
+    """rho = (v, A v)/(v, D v) after ``steps`` normalised steps of v <- D^{-1} A v (reading R4)."""
+    v = hash_vector(A.shape[0])
+    for _ in range(steps):
+        w = (A @ v) / Ddiag
+        v = w / np.linalg.norm(w)
+    return float(v @ (A @ v)) / float(v @ (Ddiag * v))
+
+
+class Hierarchy:
+    def __init__(self, A0: sp.spmatrix, d: int, p: int, n: int, levels: int = 0, nu_pre: int = 1, nu_post: int = 1):
+        self.d, self.p = d, p
+        self.ns = level_sizes(d, p, n, levels)
+        self.A = [sp.csr_matrix(A0)]
+        self.P = []
+        for l in range(len(self.ns) - 1):
+            P = prolongation(d, p, self.ns[l + 1])
+            self.P.append(P)
+            self.A.append(sp.csr_matrix(P.T @ self.A[l] @ P))      # A_{l+1} := P^T A_l P
+        self.D = [A.diagonal().copy() for A in self.A]
+        self.rho = [power_rho(self.A[l], self.D[l]) for l in range(len(self.A) - 1)]
+        self.omega = [4.0 / (3.0 * 1.05 * r) for r in self.rho]
+        self.nu_pre, self.nu_post = nu_pre, nu_post
+        self.coarse = sla.cho_factor(self.A[-1].toarray(), lower=True)
+
+    @property
+    def L(self):
+        return len(self.A) - 1
+
+    def jacobi(self, l, b, x, sweeps):
+        """sweeps x <- x + omega_l D_l^{-1} (b - A_l x)   (reading R4)."""
+        for _ in range(sweeps):
+            x = x + self.omega[l] * (b - self.A[l] @ x) / self.D[l]
+        return x
+
+    def vcycle(self, b, l: int = 0):
+        """One V-cycle for A_l e = b from a zero initial guess (steps 1-3)."""
+        if l == self.L:
+            return sla.cho_solve(self.coarse, b)
+        x = np.zeros_like(b)
+        x = self.jacobi(l, b, x, self.nu_pre)                     # step 1: pre-smoothing
+        r = b - self.A[l] @ x                                     # step 2: residual,
+        e = self.vcycle(self.P[l].T @ r, l + 1)                   #   restrict, recurse,
+        x = x + self.P[l] @ e                                     #   prolongate and correct
+        x = self.jacobi(l, b, x, self.nu_post)                    # step 3: post-smoothing
+        return x

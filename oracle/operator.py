@@ -1,0 +1,188 @@
+"""The d x d block coefficient matrix, assembled element by element by Gauss quadrature.
+
+Oracle (test infrastructure only).
+
+The product path evaluates the operator matrix-free as sums of Kronecker products;
+this oracle never uses that structure.  It assembles the sparse matrix entry by entry
+from the bilinear form, evaluating the integrand with explicit vector calculus on the
+tensor-product B-spline basis functions psi = N_{i_1}(x_1)..N_{i_d}(x_d) e_j
+(PAPER.md:409-437 (2D space V_h), 494-513 (3D)).
+
+Two bilinear forms:
+  * kind="alfven"  (the north-star operator; reading R1 in DESIGN.md): the weak form of
+        L_A u = nu u - beta lambda grad(div u) - lambda b0 x (curl curl (b0 x u))
+     with homogeneous Dirichlet conditions:
+        a(u,v) = nu (u,v) + beta lambda (div u, div v) + lambda (curl(b0 x u), curl(b0 x v)).
+    In 2D, u = (u1,u2,0), b0 = (b1,b2,0), no x3-dependence.
+  * kind="curldiv" (the paper's model operator, eq:curl-div):
+        a(u,v) = alpha (curl u, curl v) + beta (div u, div v),
+    2D curl u = d1 u2 - d2 u1.
+Unknown ordering: component-major, then lexicographic with direction 1 slowest
+("u^1 := [u^1_{2,2}, ..., u^1_{n1+p-1,n2+p-1}]").
+"""
+import itertools
+
+import numpy as np
+import scipy.sparse as sp
+
+from .bspline import element_tables
+
+
+def form_alfven(nu, beta, lam, b0):
+    return dict(kind="alfven", nu=float(nu), beta=float(beta), lam=float(lam), b0=tuple(float(v) for v in b0))
+
+
+def form_curldiv(alpha, beta):
+    return dict(kind="curldiv", alpha=float(alpha), beta=float(beta))
+
+
+def _features(form, d, Nv, G):
+    """Integrand terms for every vector basis function psi = N e_j at every quad point.
+
+    Nv[E,Q,L] scalar values, G[E,Q,L,d] scalar gradients.  Returns a list of
+    (coef, F) with F[E,Q,j,L,c]: the c-th entry of the term's vector for psi = N_L e_j;
+    a(psi_a, psi_b) = sum_terms coef * sum_Q w * F_a . F_b.
+    """
+    E, Q, L = Nv.shape
+    G3 = np.zeros((E, Q, L, 3))
+    G3[..., :d] = G
+    terms = []
+    if form["kind"] == "alfven":
+        # value: psi itself
+        val = np.zeros((E, Q, d, L, d))
+        for j in range(d):
+            val[:, :, j, :, j] = Nv
+        terms.append((form["nu"], val))
+        # div psi = d_j N
+        div = np.zeros((E, Q, d, L, 1))
+        for j in range(d):
+            div[:, :, j, :, 0] = G[..., j]
+        terms.append((form["beta"] * form["lam"], div))
+        # curl(b0 x psi) = curl(N c) with c = b0 x e_j constant: = grad N x c
+        b0 = np.zeros(3)
+        b0[: len(form["b0"])] = form["b0"]
+        cb = np.zeros((E, Q, d, L, 3))
+        for j in range(d):
+            ej = np.zeros(3)
+            ej[j] = 1.0
+            c = np.cross(b0, ej)
+            cb[:, :, j, :, :] = np.cross(G3, c[None, None, None, :])
+        terms.append((form["lam"], cb))
+    elif form["kind"] == "curldiv":
+        if d == 2:
+            curl = np.zeros((E, Q, d, L, 1))
+            curl[:, :, 0, :, 0] = -G[..., 1]      # curl(N e_1) = -d2 N
+            curl[:, :, 1, :, 0] = G[..., 0]       # curl(N e_2) =  d1 N
+        else:
+            curl = np.zeros((E, Q, d, L, 3))
+            for j in range(d):
+                ej = np.zeros(3)
+                ej[j] = 1.0
+                curl[:, :, j, :, :] = np.cross(G3, ej[None, None, None, :])  # curl(N e_j) = grad N x e_j
+        terms.append((form["alpha"], curl))
+        div = np.zeros((E, Q, d, L, 1))
+        for j in range(d):
+            div[:, :, j, :, 0] = G[..., j]
+        terms.append((form["beta"], div))
+    else:
+        raise ValueError(form["kind"])
+    return terms
+
+
+class Discretization:
+    """Tensor-product B-spline space of degree p on n^d uniform elements, Dirichlet."""
+
+    def __init__(self, d: int, p: int, n: int):
+        self.d, self.p, self.n = d, p, n
+        self.m = n + p - 2
+        self.nscal = self.m ** d
+        self.ndof = d * self.nscal
+        self.q = p + 1
+        self._tab = element_tables(p, n, self.q)
+
+    def _element_data(self, elems):
+        """Scalar basis values/gradients on a batch of elements (rows of multi-indices)."""
+        d, p, q = self.d, self.p, self.q
+        _, wq, B, D = self._tab
+        E = len(elems)
+        # quadrature points / local functions as tensor products over directions
+        qidx = np.array(list(itertools.product(range(q), repeat=d)))          # (Q,d)
+        lidx = np.array(list(itertools.product(range(p + 1), repeat=d)))      # (L,d)
+        Q, L = len(qidx), len(lidx)
+        Nv = np.ones((E, Q, L))
+        G = np.ones((E, Q, L, d))
+        W = np.ones((E, Q))
+        for l in range(d):
+            el = elems[:, l]
+            b = B[el][:, qidx[:, l], :][:, :, lidx[:, l]]     # (E,Q,L)
+            db = D[el][:, qidx[:, l], :][:, :, lidx[:, l]]
+            W *= wq[el][:, qidx[:, l]]
+            Nv = Nv * b
+            for c in range(d):
+                G[..., c] *= db if c == l else b
+        # global scalar interior index of each local function (-1 if a removed boundary spline)
+        gidx = np.zeros((E, L), dtype=np.int64)
+        valid = np.ones((E, L), dtype=bool)
+        for l in range(d):
+            i1 = elems[:, l][:, None] + lidx[None, :, l] + 1       # 1-based spline index
+            k = i1 - 2
+            valid &= (k >= 0) & (k < self.m)
+            gidx = gidx * self.m + np.clip(k, 0, self.m - 1)
+        return W, Nv, G, gidx, valid
+
+    def local_matrices(self, form, elems):
+        W, Nv, G, gidx, valid = self._element_data(elems)
+        terms = _features(form, self.d, Nv, G)
+        E, Q, L = Nv.shape
+        d = self.d
+        K = np.zeros((E, d * L, d * L))
+        for coef, F in terms:
+            if coef == 0.0:
+                continue
+            Fr = F.reshape(E, Q, d * L, F.shape[-1])
+            K += coef * np.einsum("eq,eqac,eqbc->eab", W, Fr, Fr, optimize=True)
+        # global vector dof index: component j, scalar index
+        gv = (np.arange(d)[None, :, None] * self.nscal + gidx[:, None, :]).reshape(E, d * L)
+        vv = np.broadcast_to(valid[:, None, :], (E, d, L)).reshape(E, d * L)
+        return K, gv, vv
+
+    def assemble(self, form, chunk=4096) -> sp.csr_matrix:
+        """The full sparse matrix (test sizes only)."""
+        elems = np.array(list(itertools.product(range(self.n), repeat=self.d)))
+        rows, cols, vals = [], [], []
+        A = sp.csr_matrix((self.ndof, self.ndof))
+        for s in range(0, len(elems), chunk):
+            K, gv, vv = self.local_matrices(form, elems[s: s + chunk])
+            msk = vv[:, :, None] & vv[:, None, :]
+            r = np.broadcast_to(gv[:, :, None], K.shape)[msk]
+            c = np.broadcast_to(gv[:, None, :], K.shape)[msk]
+            A = A + sp.coo_matrix((K[msk], (r, c)), shape=(self.ndof, self.ndof)).tocsr()
+        A.sum_duplicates()
+        return A
+
+    def support_elements(self, dof):
+        """Elements on which the basis function of vector dof ``dof`` is nonzero."""
+        flat = dof % self.nscal
+        ks = []
+        for l in range(self.d):
+            ks.append(flat // self.m ** (self.d - 1 - l) % self.m)
+        rng = []
+        for k in ks:
+            i = k + 2                      # 1-based spline index
+            rng.append(range(max(0, i - self.p - 1), min(self.n, i)))
+        return np.array(list(itertools.product(*rng)), dtype=np.int64)
+
+    def sampled_apply(self, form, x, dofs):
+        """(A x)[dofs] computed row by row from the element integrals (any problem size)."""
+        out = np.zeros(len(dofs))
+        for t, I in enumerate(dofs):
+            elems = self.support_elements(int(I))
+            K, gv, vv = self.local_matrices(form, elems)
+            s = 0.0
+            for e in range(len(elems)):
+                rows = np.nonzero((gv[e] == I) & vv[e])[0]
+                for r in rows:
+                    cm = vv[e]
+                    s += float(np.dot(K[e, r, cm], x[gv[e, cm]]))
+            out[t] = s
+        return out

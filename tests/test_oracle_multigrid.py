@@ -1,0 +1,122 @@
+"""Pins of oracle/transfer.py, oracle/multigrid.py and oracle/krylov.py (no GPU)."""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import scipy.sparse as sp
+import scipy.sparse.linalg as spl
+
+import inputs
+from oracle import bspline as bs
+from oracle.krylov import pcg
+from oracle.multigrid import Hierarchy, level_sizes, power_rho
+from oracle.operator import Discretization, form_alfven
+from oracle.transfer import prolongation, prolongation_1d
+
+
+@pytest.mark.parametrize("p,nc", [(1, 3), (2, 4), (3, 5), (4, 6), (5, 7)])
+def test_prolongation_reproduces_coarse_splines(p, nc):
+    C = prolongation_1d(p, nc, full=True)
+    for x in np.random.default_rng(p).uniform(0, 1, 20):
+        assert np.max(np.abs(bs.basis(p, 2 * nc, x) @ C - bs.basis(p, nc, x))) < 1e-13
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_prolongation_central_columns_are_binomial(p):
+    # two-scale relation of the cardinal B-spline: phi_p(t) = 2^-p sum_k C(p+1,k) phi_p(2t-k)
+    nc = 4 * p + 4
+    C = prolongation_1d(p, nc, full=True)
+    j = nc // 2 + p // 2          # a central coarse spline (1-based j+1)
+    col = C[:, j]
+    nz = col[np.abs(col) > 1e-12]
+    ref = np.array([math.comb(p + 1, k) for k in range(p + 2)]) / 2 ** p
+    assert len(nz) == p + 2 and np.max(np.abs(nz - ref)) < 1e-13
+
+
+@pytest.mark.parametrize("d,p,nc", [(2, 2, 3), (2, 3, 4), (3, 2, 2), (3, 3, 2)])
+def test_galerkin_coarse_operator_equals_coarse_discretization(d, p, nc):
+    # nested spaces: P^T A_h P = A_{2h}  (A_{l+1} := P^T A_l P)
+    f = form_alfven(0.2, 0.05, 1.0, np.ones(d) / math.sqrt(d))
+    Af = Discretization(d, p, 2 * nc).assemble(f)
+    Ac = Discretization(d, p, nc).assemble(f)
+    P = prolongation(d, p, nc)
+    G = (P.T @ Af @ P).toarray()
+    assert np.max(np.abs(G - Ac.toarray())) < 1e-13 * np.max(np.abs(G))
+
+
+def test_level_rule():
+    assert level_sizes(2, 2, 16, 2) == [16, 8]
+    assert level_sizes(3, 4, 160) == [160, 80, 40, 20, 10, 5]
+    assert level_sizes(2, 3, 256) == [256, 128, 64, 32, 16]
+    assert level_sizes(3, 3, 64) == [64, 32, 16, 8, 4]
+    assert level_sizes(2, 5, 1024)[-1] == 16
+
+
+def _setup(d=2, p=2, n=8, levels=0, nu=1.0, beta=0.05, b0=(0.6, 0.8)):
+    A = Discretization(d, p, n).assemble(form_alfven(nu, beta, 1.0, b0))
+    return A, Hierarchy(A, d, p, n, levels)
+
+
+def test_power_rho_close_to_true_lambda_max():
+    A, H = _setup()
+    D = A.diagonal()
+    lam = sla.eigh(A.toarray(), np.diag(D), eigvals_only=True)[-1]
+    rho = power_rho(A, D)
+    assert 0.85 * lam <= rho <= lam * (1 + 1e-12)
+
+
+def test_vcycle_symmetric_positive_definite():
+    A, H = _setup(n=8, levels=2)
+    N = A.shape[0]
+    B = np.column_stack([H.vcycle(e) for e in np.eye(N)])
+    assert np.max(np.abs(B - B.T)) < 1e-10 * np.max(np.abs(B))
+    assert np.linalg.eigvalsh(0.5 * (B + B.T))[0] > 0
+    # two-grid error propagation I - B A is a contraction in the A-norm
+    E = np.eye(N) - B @ A.toarray()
+    Lc = np.linalg.cholesky(A.toarray())
+    assert np.linalg.norm(Lc.T @ E @ np.linalg.inv(Lc.T), 2) < 1.0
+
+
+def test_coarse_correction_exact_on_coarse_space():
+    # with no smoothing, x = P A_c^{-1} P^T b; for b = A P y this returns P y
+    A, H = _setup(n=8, levels=2)
+    H.nu_pre = H.nu_post = 0
+    y = np.random.default_rng(1).standard_normal(H.A[1].shape[0])
+    b = A @ (H.P[0] @ y)
+    assert np.max(np.abs(H.vcycle(b) - H.P[0] @ y)) < 1e-10 * np.max(np.abs(H.P[0] @ y))
+
+
+def test_jacobi_fixed_point():
+    A, H = _setup(levels=2)
+    x = np.random.default_rng(2).standard_normal(A.shape[0])
+    assert np.max(np.abs(H.jacobi(0, A @ x, x, 3) - x)) < 1e-13 * np.max(np.abs(x))
+
+
+def test_pcg_matches_direct_solve_and_counts():
+    A, H = _setup(n=16, levels=0)
+    b = np.random.default_rng(3).uniform(-1, 1, A.shape[0])
+    x, it, hist = pcg(A, b, H.vcycle, 1e-12, 500)
+    xs = spl.spsolve(A.tocsc(), b)
+    assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 1e-8
+    assert hist[-1] < 1e-12 and all(h >= 1e-12 for h in hist[:-1])
+    # exact preconditioner: one iteration
+    lu = spl.splu(A.tocsc())
+    _, it1, _ = pcg(A, b, lu.solve, 1e-10, 10)
+    assert it1 == 1
+    # k distinct eigenvalues -> at most k iterations (Krylov theory)
+    Dm = sp.diags(np.repeat([1.0, 2.0, 5.0, 9.0], 25))
+    _, it4, _ = pcg(Dm, np.ones(100), lambda r: r, 1e-12, 50)
+    assert it4 <= 4
+    _, it0, _ = pcg(A, np.zeros(A.shape[0]), H.vcycle, 1e-8, 10)
+    assert it0 == 0
+
+
+def test_config0_solves():
+    c = inputs.config(0)
+    A = Discretization(c.dim, c.p, c.n).assemble(form_alfven(c.nu, c.beta, c.lam, c.b0))
+    H = Hierarchy(A, c.dim, c.p, c.n, c.levels)
+    b = inputs.rhs(c)
+    x, it, hist = pcg(A, b, H.vcycle, c.tol, 1000)
+    assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) < 2 * c.tol
+    assert it < 100

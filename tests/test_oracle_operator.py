@@ -1,0 +1,127 @@
+"""Pins of oracle/operator.py (element-wise assembly) against the paper's printed matrices,
+vector-calculus identities and the spectral symbol (no GPU)."""
+import numpy as np
+import pytest
+
+from oracle import matrices1d as m1
+from oracle import symbol as sy
+from oracle.operator import Discretization, form_alfven, form_curldiv
+
+K = np.kron
+
+
+def k3(a, b, c):
+    return K(K(a, b), c)
+
+
+def paper_2d(p, n, alpha, beta):
+    """eq:matr_Amu, typed from the paper."""
+    M, A, S = m1.matrices(p, n)
+    AT = A.T
+    curl = np.block([[K(M, S), -K(AT, A)], [-K(A, AT), K(S, M)]])
+    div = np.block([[K(S, M), K(A, AT)], [K(AT, A), K(M, S)]])
+    return alpha * curl + beta * div, M
+
+
+def paper_3d(p, n, alpha, beta):
+    """eq:matr_Amu3D, typed from the paper."""
+    M, A, S = m1.matrices(p, n)
+    AT = A.T
+    curl = np.block([
+        [k3(M, M, S) + k3(M, S, M), -k3(AT, A, M), -k3(AT, M, A)],
+        [-k3(A, AT, M), k3(S, M, M) + k3(M, M, S), -k3(M, AT, A)],
+        [-k3(A, M, AT), -k3(M, A, AT), k3(S, M, M) + k3(M, S, M)]])
+    div = np.block([
+        [k3(S, M, M), k3(A, AT, M), k3(A, M, AT)],
+        [k3(AT, A, M), k3(M, S, M), k3(M, A, AT)],
+        [k3(AT, M, A), k3(M, AT, A), k3(M, M, S)]])
+    return alpha * curl + beta * div, M
+
+
+@pytest.mark.parametrize("p,n,alpha,beta", [(1, 6, 1.0, 0.5), (2, 6, 1.0, 0.01), (3, 7, 0.7, 0.2), (4, 8, 1.0, 1e-3)])
+def test_curldiv_2d_equals_paper_kronecker_form(p, n, alpha, beta):
+    ref, _ = paper_2d(p, n, alpha, beta)
+    got = Discretization(2, p, n).assemble(form_curldiv(alpha, beta)).toarray()
+    assert np.max(np.abs(got - ref)) < 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("p,n,alpha,beta", [(1, 4, 1.0, 0.5), (2, 4, 1.0, 0.01), (3, 5, 0.3, 2.0)])
+def test_curldiv_3d_equals_paper_kronecker_form(p, n, alpha, beta):
+    ref, _ = paper_3d(p, n, alpha, beta)
+    got = Discretization(3, p, n).assemble(form_curldiv(alpha, beta)).toarray()
+    assert np.max(np.abs(got - ref)) < 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("d,p,n", [(2, 2, 6), (2, 3, 7), (3, 2, 4), (3, 3, 4)])
+def test_alfven_special_cases(d, p, n):
+    disc = Discretization(d, p, n)
+    M = m1.matrices(p, n)[0]
+    Ms = M if d == 2 else K(M, M)
+    if d == 3:
+        Ms = K(M, Ms)
+    else:
+        Ms = K(M, M)
+    # nu-only: nu (u, v) = nu I_d (x) M (x) .. (x) M
+    got = disc.assemble(form_alfven(0.37, 0.0, 0.0, [1.0] + [0.0] * (d - 1))).toarray()
+    assert np.max(np.abs(got - 0.37 * K(np.eye(d), Ms))) < 1e-15
+    # b0 = 0 leaves beta*lambda (div, div) = paper's A^div (eq:matr_Adiv / Amu3D beta part)
+    ref = (paper_2d if d == 2 else paper_3d)(p, n, 0.0, 1.0)[0]
+    got = disc.assemble(form_alfven(0.0, 0.5, 2.0, [0.0] * d)).toarray()
+    assert np.max(np.abs(got - ref)) < 1e-13 * np.max(np.abs(ref))
+    # sum over b0 = e_k of lambda (curl(b0 x u), curl(b0 x v)) = (grad u, grad v) + (div u, div v)
+    #   = (curl u, curl v) + d-1 ... : 2D -> curldiv(1, 1), 3D -> curldiv(1, 2)  (H^1_0 identity)
+    s = sum(disc.assemble(form_alfven(0.0, 0.0, 1.0, np.eye(d)[k])).toarray() for k in range(d))
+    ref = (paper_2d if d == 2 else paper_3d)(p, n, 1.0, float(d - 1))[0]
+    assert np.max(np.abs(s - ref)) < 1e-13 * np.max(np.abs(ref))
+
+
+def test_alfven_2d_b0_e1_is_laplacian_on_u2():
+    # b0=(1,0): curl(b0 x u) = (d2 u2, -d1 u2): lambda (grad u2, grad v2) = lambda (S(x)M + M(x)S) on block (2,2)
+    p, n = 3, 7
+    M, A, S = m1.matrices(p, n)
+    got = Discretization(2, p, n).assemble(form_alfven(0.0, 0.0, 1.5, (1.0, 0.0))).toarray()
+    m2 = (n + p - 2) ** 2
+    ref = np.zeros_like(got)
+    ref[m2:, m2:] = 1.5 * (K(S, M) + K(M, S))
+    assert np.max(np.abs(got - ref)) < 1e-13
+
+
+@pytest.mark.parametrize("cfg", [(2, 3, 6, 1e-2, 1e-3, 1.0, (2 ** -0.5, 2 ** -0.5)),
+                                 (3, 2, 4, 1e-3, 1e-4, 1.0, (3 ** -0.5,) * 3)])
+def test_alfven_symmetric_positive_definite_and_linear(cfg):
+    d, p, n, nu, beta, lam, b0 = cfg
+    disc = Discretization(d, p, n)
+    A = disc.assemble(form_alfven(nu, beta, lam, b0)).toarray()
+    assert np.max(np.abs(A - A.T)) < 1e-15 * np.max(np.abs(A)) * 10
+    assert np.linalg.eigvalsh(A)[0] > 0
+    A2 = (disc.assemble(form_alfven(nu, 0, 0, b0)) + disc.assemble(form_alfven(0, beta, lam, [0] * d))
+          + disc.assemble(form_alfven(0, 0, lam, b0))).toarray()
+    assert np.max(np.abs(A - A2)) < 1e-14 * np.max(np.abs(A))
+
+
+def test_sampled_apply_equals_assembled_rows():
+    d, p, n = 3, 3, 5
+    disc = Discretization(d, p, n)
+    f = form_alfven(0.3, 0.1, 1.0, (0.6, 0.0, 0.8))
+    A = disc.assemble(f)
+    x = np.random.default_rng(5).standard_normal(disc.ndof)
+    dofs = [0, 7, disc.nscal + 11, disc.ndof - 1, 2 * disc.nscal + 31]
+    assert np.max(np.abs(disc.sampled_apply(f, x, dofs) - (A @ x)[dofs])) < 1e-13
+
+
+@pytest.mark.parametrize("beta", [0.5, 0.01])
+def test_2d_spectrum_follows_symbol(beta):
+    # Theorem 5.1 / Fig. 1: eigenvalues of A^{p,alpha,beta}_n vs sorted symbol samples
+    p, n, alpha = 3, 40, 1.0              # the paper's Fig. 1 setting
+    A = Discretization(2, p, n).assemble(form_curldiv(alpha, beta)).toarray()
+    ev = np.sort(np.linalg.eigvalsh(A))
+    m = n + p - 2
+    T1, T2 = sy.grid(m, 2)
+    lam = np.linalg.eigvalsh(sy.symbol_f(p, alpha, beta, (T1, T2)))
+    samp = np.sort(lam.ravel())
+    rel = np.abs(ev - samp) / np.maximum(samp, 1e-3 * samp.max())
+    # rank-aligned agreement "up to some outliers"; the small end is the most sensitive
+    assert np.mean(rel < 0.1) > (0.95 if beta == 0.5 else 0.75)
+    if beta == 0.01:   # "about half of the spectrum is almost zero"
+        frac = np.mean(ev < 0.05 * ev.max())
+        assert 0.45 < frac < 0.55
