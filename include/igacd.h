@@ -1,0 +1,122 @@
+/*
+ * igacd.h -- C ABI of the B200 IgA curl-div solver (libigacd.so).
+ *
+ * Operator (reading R1): the Galerkin matrix of the Alfven-like operator
+ *   L_A u = nu u - beta*lambda grad(div u) - lambda b0 x (curl curl (b0 x u))
+ * with homogeneous Dirichlet conditions imposed strongly, discretised with
+ * tensor-product B-splines of degree p on n uniform elements per direction of (0,1)^d,
+ * d = 2 or 3:
+ *   a(u,v) = nu (u,v) + beta*lambda (div u, div v) + lambda (curl(b0 x u), curl(b0 x v)).
+ *
+ * VECTORS.  Every vector argument is a plain array of doubles of length igacd_ndof(h, level)
+ * = d * m^d, m = n_level + p - 2 (the interior B-splines N_2..N_{n+p-1}),
+ * component-major, then lexicographic with direction 1 slowest:
+ *   index(j, k_1, .., k_d) = j*m^d + (..(k_1*m + k_2)*m + ..) + k_d.
+ * Unless a name says _host, pointers are CUDA DEVICE pointers owned by the caller; the
+ * library never frees them.  Input and output buffers must not alias unless stated.
+ *
+ * STREAMS.  `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ * All work is enqueued on it; functions return without synchronising except where stated
+ * (igacd_create, igacd_solve, igacd_solve_host, queries).
+ *
+ * ERRORS.  Every function returns an int status: 0 = success, < 0 = failure
+ * (IGACD_E_* below).  igacd_last_error() returns a thread-local message for the last failure.
+ * A failure leaves caller-owned buffers in an unspecified state; the handle stays valid
+ * unless igacd_create itself failed (then *out is NULL).
+ */
+#ifndef IGACD_H
+#define IGACD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IGACD_OK 0
+#define IGACD_E_ARG (-1)      /* invalid argument (dimension, degree, size, null pointer)  */
+#define IGACD_E_CUDA (-2)     /* a CUDA runtime call or kernel launch failed                */
+#define IGACD_E_NOTSPD (-3)   /* coarse Cholesky met a non-positive pivot                    */
+#define IGACD_E_NOCONV (-4)   /* igacd_solve reached maxit without the requested residual   */
+
+typedef struct igacd_handle_s* igacd_handle;
+
+/* Build the hierarchy for the operator above.
+ *   dim    2 or 3;   p  degree, 1 <= p <= 6;   n  elements per direction, n + p - 2 >= 1
+ *   nu, beta, lambda  >= 0 (nu > 0, beta in (1e-4, 1e-1], lambda = V_A dt)
+ *   b0     host array of `dim` doubles, used as given (the configs pass unit vectors)
+ *   levels 0 = automatic coarsening rule (reading R6), else exactly `levels` levels
+ *   nu_pre, nu_post  damped-Jacobi sweeps before / after the coarse correction (reading R4)
+ * Work: 1D assembly (R1) and knot-insertion (R3) kernels, coarse inverse (R5), smoother
+ * parameters by power iteration (R4).  Synchronises `stream`.  Owns all its device memory. */
+int igacd_create(igacd_handle* out, int dim, int p, int n, double nu, double beta, double lambda,
+                 const double* b0, int levels, int nu_pre, int nu_post, void* stream);
+
+/* Same, for a general constant-coefficient form a(u,v) = sum_ij mass[i][j] (u_j, v_i)
+ *   + sum_{i,b,j,a} K[((i*dim+b)*dim+j)*dim+a] (d_a u_j, d_b v_i)   (test (i,b), trial (j,a),
+ * directions 0-based, host arrays of dim^2 and dim^4 doubles).  The matrix must be SPD.
+ * Used for the paper's model form alpha curl-curl + beta div-div (eq:curl-div). */
+int igacd_create_form(igacd_handle* out, int dim, int p, int n, const double* mass, const double* K,
+                      int levels, int nu_pre, int nu_post, void* stream);
+
+int igacd_destroy(igacd_handle h);
+
+/* Queries (host values; no device work). */
+int igacd_get_info(igacd_handle h, int* dim, int* p, int* levels);
+int igacd_num_levels(igacd_handle h, int* levels);
+int igacd_level_n(igacd_handle h, int level, int* n);
+int igacd_ndof(igacd_handle h, int level, size_t* ndof);
+int igacd_smoother_omega(igacd_handle h, int level, double* omega, double* rho);
+
+/* y = A_level x   (R2).  x, y device, length igacd_ndof(h, level); x != y. */
+int igacd_apply(igacd_handle h, int level, const double* x, double* y, void* stream);
+
+/* r = b - A_level x   (R2 with the residual epilogue). */
+int igacd_residual(igacd_handle h, int level, const double* b, const double* x, double* r, void* stream);
+
+/* `sweeps` damped-Jacobi sweeps x <- x + omega_l D_l^{-1} (b - A_l x) in place on x (R4).
+ * omega_l as reported by igacd_smoother_omega unless omega > 0 is given (then used as is). */
+int igacd_smooth(igacd_handle h, int level, const double* b, double* x, int sweeps, double omega, void* stream);
+
+/* x_coarse = P_level^T x_fine   (R3, restriction to level+1). */
+int igacd_restrict(igacd_handle h, int level, const double* x_fine, double* x_coarse, void* stream);
+
+/* x_fine = P_level x_coarse (accumulate == 0) or x_fine += P_level x_coarse (accumulate != 0). */
+int igacd_prolong(igacd_handle h, int level, const double* x_coarse, double* x_fine, int accumulate, void* stream);
+
+/* One V-cycle from a zero initial guess: x = B b, the preconditioner action (R6). */
+int igacd_vcycle(igacd_handle h, const double* b, double* x, void* stream);
+
+/* PCG with the V-cycle preconditioner, zero initial guess, stop when
+ * ||r_k||_2 / ||r_0||_2 < tol or after maxit iterations (R7).
+ * iters, relres: host outputs (may be NULL).  Synchronises `stream`.
+ * Returns IGACD_E_NOCONV (x still written) when maxit is reached. */
+int igacd_solve(igacd_handle h, const double* b, double* x, double tol, int maxit, int* iters,
+                double* relres, void* stream);
+
+/* As igacd_solve with HOST b and x (pinned or pageable); the host<->device copies are
+ * part of the call. */
+int igacd_solve_host(igacd_handle h, const double* b_host, double* x_host, double tol, int maxit,
+                     int* iters, double* relres, void* stream);
+
+/* Debug/parity access (host outputs).
+ * igacd_get_band: the level's 1D factors in band storage, each m*(2p+1) doubles with
+ *   F[k][k+o] at [k*(2p+1) + o + p] (zero outside the matrix); which = 0 M, 1 A, 2 S.
+ * igacd_get_prolongation: dense (m_level x m_{level+1}) 1D knot-insertion matrix, row-major. */
+int igacd_get_band(igacd_handle h, int level, int which, double* band_host);
+int igacd_get_prolongation(igacd_handle h, int level, double* P_host);
+
+/* Instrumentation: kernel launch counter (all of this handle's kernels) and, when enabled,
+ * CUDA-event timing of the level-0 operator-apply kernels issued inside igacd_solve. */
+int igacd_set_profiling(igacd_handle h, int enable);
+int igacd_get_profile(igacd_handle h, long long* launches, long long* apply_launches, double* apply_ms);
+int igacd_reset_profile(igacd_handle h);
+
+const char* igacd_last_error(void);
+const char* igacd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGACD_H */

@@ -98,12 +98,23 @@ class Discretization:
         self.nscal = self.m ** d
         self.ndof = d * self.nscal
         self.q = p + 1
-        self._tab = element_tables(p, n, self.q)
+        self._cache = {}      # 1D element tables, computed on demand (large n: few elements used)
+
+    def _tables(self, els):
+        """(wq, B, D) rows for the listed 1D elements (see bspline.element_tables)."""
+        miss = sorted(set(int(e) for e in els) - self._cache.keys())
+        if miss:
+            _, wq, B, D = element_tables(self.p, self.n, self.q, miss)
+            for k, e in enumerate(miss):
+                self._cache[e] = (wq[k], B[k], D[k])
+        wq = np.array([self._cache[int(e)][0] for e in els])
+        B = np.array([self._cache[int(e)][1] for e in els])
+        D = np.array([self._cache[int(e)][2] for e in els])
+        return wq, B, D
 
     def _element_data(self, elems):
         """Scalar basis values/gradients on a batch of elements (rows of multi-indices)."""
         d, p, q = self.d, self.p, self.q
-        _, wq, B, D = self._tab
         E = len(elems)
         # quadrature points / local functions as tensor products over directions
         qidx = np.array(list(itertools.product(range(q), repeat=d)))          # (Q,d)
@@ -113,10 +124,10 @@ class Discretization:
         G = np.ones((E, Q, L, d))
         W = np.ones((E, Q))
         for l in range(d):
-            el = elems[:, l]
-            b = B[el][:, qidx[:, l], :][:, :, lidx[:, l]]     # (E,Q,L)
-            db = D[el][:, qidx[:, l], :][:, :, lidx[:, l]]
-            W *= wq[el][:, qidx[:, l]]
+            wq, B, D = self._tables(elems[:, l])
+            b = B[:, qidx[:, l], :][:, :, lidx[:, l]]     # (E,Q,L)
+            db = D[:, qidx[:, l], :][:, :, lidx[:, l]]
+            W *= wq[:, qidx[:, l]]
             Nv = Nv * b
             for c in range(d):
                 G[..., c] *= db if c == l else b
@@ -173,16 +184,34 @@ class Discretization:
         return np.array(list(itertools.product(*rng)), dtype=np.int64)
 
     def sampled_apply(self, form, x, dofs):
-        """(A x)[dofs] computed row by row from the element integrals (any problem size)."""
+        """(A x)[dofs] computed row by row from the element integrals (any problem size).
+
+        Per sampled dof only the local-matrix row of that basis function is formed:
+        row_e = sum_terms coef sum_q w F_row(q) . F(q) over the elements of its support.
+        """
         out = np.zeros(len(dofs))
+        d = self.d
         for t, I in enumerate(dofs):
-            elems = self.support_elements(int(I))
-            K, gv, vv = self.local_matrices(form, elems)
+            I = int(I)
+            elems = self.support_elements(I)
+            W, Nv, G, gidx, valid = self._element_data(elems)
+            terms = _features(form, d, Nv, G)
+            E, Q, L = Nv.shape
+            gv = (np.arange(d)[None, :, None] * self.nscal + gidx[:, None, :]).reshape(E, d * L)
+            vv = np.broadcast_to(valid[:, None, :], (E, d, L)).reshape(E, d * L)
             s = 0.0
-            for e in range(len(elems)):
+            for e in range(E):
                 rows = np.nonzero((gv[e] == I) & vv[e])[0]
-                for r in rows:
-                    cm = vv[e]
-                    s += float(np.dot(K[e, r, cm], x[gv[e, cm]]))
+                if len(rows) == 0:
+                    continue
+                r = rows[0]
+                krow = np.zeros(d * L)
+                for coef, F in terms:
+                    if coef == 0.0:
+                        continue
+                    Fr = F[e].reshape(Q, d * L, F.shape[-1])
+                    krow += coef * np.einsum("q,qc,qbc->b", W[e], Fr[:, r, :], Fr)
+                cm = vv[e]
+                s += float(np.dot(krow[cm], x[gv[e, cm]]))
             out[t] = s
         return out

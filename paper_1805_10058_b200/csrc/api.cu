@@ -1,0 +1,579 @@
+// C ABI of libigacd (include/igacd.h): setup, V-cycle (R6) and PCG (R7) drivers.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace igacd {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+// ---- operator coefficients ------------------------------------------------------------
+// Reading R1: a(u,v) = nu (u,v) + beta lambda (div u, div v) + lambda (curl(b0 x u), curl(b0 x v)).
+// For constant b0, curl(b0 x u) = b0 div u - (b0 . grad) u, so with test (i,b), trial (j,a)
+//   K[(i,b),(j,a)] = beta lambda d_ib d_ja + lambda sum_m (b0_m d_ib - b0_b d_im)(b0_m d_ja - b0_a d_jm)
+//                  = (beta lambda + lambda |b0|^2) d_ib d_ja
+//                    + lambda (-d_ib b0_j b0_a - d_ja b0_i b0_b + d_ij b0_a b0_b).
+// In 2D (u3 = 0, d/dx3 = 0, b0 in the plane) the same formula holds on indices {0,1}.
+static void alfven_form(int d, double nu, double beta, double lam, const double* b0, double* mass, double* K) {
+  double bb = 0.0;
+  for (int a = 0; a < d; ++a) bb += b0[a] * b0[a];
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) mass[i * d + j] = (i == j) ? nu : 0.0;
+  for (int i = 0; i < d; ++i)
+    for (int b = 0; b < d; ++b)
+      for (int j = 0; j < d; ++j)
+        for (int a = 0; a < d; ++a) {
+          const double dib = i == b, dja = j == a, dij = i == j;
+          K[((i * d + b) * d + j) * d + a] = (beta * lam + lam * bb) * dib * dja +
+                                            lam * (-dib * b0[j] * b0[a] - dja * b0[i] * b0[b] + dij * b0[a] * b0[b]);
+        }
+}
+
+// Kronecker patterns (internal.cuh Coef) of a(u,v) = sum mass (u_j,v_i) + sum K (d_a u_j, d_b v_i).
+// 1D factor per direction l: M if l not in {a,b}; S if l = a = b; A if l = a != b (derivative on
+// the trial function, A_kj = int N_k N_j'); A^T = -A if l = b != a.  Hence the pattern A(x)A on
+// the pair {k,l} collects -(K[(i,l),(j,k)] + K[(i,k),(j,l)]).
+static Coef patterns(int d, const double* mass, const double* K) {
+  Coef c;
+  std::memset(&c, 0, sizeof(c));
+  auto Kf = [&](int i, int b, int j, int a) { return K[((i * d + b) * d + j) * d + a]; };
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) {
+      c.mass[i][j] = mass[i * d + j];
+      for (int l = 0; l < d; ++l) c.S[l][i][j] = Kf(i, l, j, l);
+      int q = 0;
+      for (int k = 0; k < d; ++k)
+        for (int l = k + 1; l < d; ++l, ++q) c.AA[q][i][j] = -(Kf(i, l, j, k) + Kf(i, k, j, l));
+    }
+  return c;
+}
+
+// Reading R6: n_{l+1} = n_l/2 while n_l is even, n_l/2 + p - 2 >= 1 and d (n_l+p-2)^d > NCOARSE_MAX.
+static std::vector<int> level_sizes(int d, int p, int n, int levels) {
+  std::vector<int> ns{n};
+  auto big = [&](int nn) {
+    double m = nn + p - 2;
+    return d * std::pow(m, d) > NCOARSE_MAX;
+  };
+  if (levels > 0) {
+    for (int l = 1; l < levels; ++l) {
+      if (ns.back() % 2 || ns.back() / 2 + p - 2 < 1)
+        throw Error{IGACD_E_ARG, "requested number of levels impossible for this n and p"};
+      ns.push_back(ns.back() / 2);
+    }
+    return ns;
+  }
+  while (ns.back() % 2 == 0 && ns.back() / 2 + p - 2 >= 1 && big(ns.back())) ns.push_back(ns.back() / 2);
+  return ns;
+}
+
+static void destroy_handle(Handle* h) {
+  if (!h) return;
+  for (auto& L : h->lv) {
+    for (int f = 0; f < 3; ++f) cudaFree(L.band[f]);
+    cudaFree(L.b);
+    cudaFree(L.x);
+    cudaFree(L.t);
+    cudaFree(L.r);
+  }
+  for (auto& T : h->tr) {
+    cudaFree(T.p_start);
+    cudaFree(T.p_w);
+    cudaFree(T.r_start);
+    cudaFree(T.r_w);
+  }
+  cudaFree(h->cinv);
+  cudaFree(h->scratch0);
+  cudaFree(h->scratch1);
+  cudaFree(h->partial);
+  cudaFree(h->scal);
+  if (h->hscal) cudaFreeHost(h->hscal);
+  cudaFree(h->pr);
+  cudaFree(h->pz);
+  cudaFree(h->pp);
+  cudaFree(h->pq);
+  cudaFree(h->px);
+  cudaFree(h->pb);
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  for (auto& pr : h->ev_pending) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  delete h;
+}
+
+enum Slot { S_NORM = 0, S_PQ = 1, S_RR = 2, S_RZ0 = 3, S_RZ1 = 4, S_A = 5, S_B = 6, NSLOT = 8 };
+
+static double reduce_to_host(Handle& h, int nparts, int slot, cudaStream_t s) {
+  launch_finalize(h, h.partial, nparts, h.scal + slot, s);
+  IGACD_CUDA(cudaMemcpyAsync(h.hscal + slot, h.scal + slot, sizeof(double), cudaMemcpyDeviceToHost, s));
+  IGACD_CUDA(cudaStreamSynchronize(s));
+  return h.hscal[slot];
+}
+
+static void estimate_omega(Handle& h, int l, cudaStream_t s) {
+  Level& L = h.lv[l];
+  double* v = L.x;
+  double* w = L.t;
+  launch_hash_vector(h, v, L.ndof, s);
+  Epi ep{};
+  ep.partial = h.partial;
+  for (int it = 0; it < POWER_STEPS; ++it) {
+    const int np = launch_operator(h, l, v, w, EPI_DINV, DOT_OUT_OUT, ep, s);
+    launch_finalize(h, h.partial, np, h.scal + S_NORM, s);
+    launch_scale(h, w, h.scal + S_NORM, nullptr, L.ndof, s);
+    std::swap(v, w);
+  }
+  const int np = launch_operator(h, l, v, w, EPI_APPLY, DOT_X_OUT, ep, s);
+  const double vAv = reduce_to_host(h, np, S_A, s);
+  launch_dvdot(h, l, v, h.partial, s);
+  const double vDv = reduce_to_host(h, vec_ctas(L.ndof), S_B, s);
+  L.rho = vAv / vDv;
+  L.omega = 4.0 / (3.0 * 1.05 * L.rho);
+}
+
+static Handle* create_impl(int dim, int p, int n, const double* mass, const double* K, int levels, int nu_pre,
+                           int nu_post, cudaStream_t s) {
+  if (dim != 2 && dim != 3) throw Error{IGACD_E_ARG, "dim must be 2 or 3"};
+  if (p < 1 || p > MAXP) throw Error{IGACD_E_ARG, "p must be in [1, 6]"};
+  if (n < 1 || n + p - 2 < 1) throw Error{IGACD_E_ARG, "need n >= 1 and n + p - 2 >= 1"};
+  if (nu_pre < 0 || nu_post < 0) throw Error{IGACD_E_ARG, "negative sweep count"};
+  Handle* h = new Handle();
+  try {
+    h->dim = dim;
+    h->p = p;
+    h->nu_pre = nu_pre;
+    h->nu_post = nu_post;
+    h->stream = s;
+    h->coef = patterns(dim, mass, K);
+    const std::vector<int> ns = level_sizes(dim, p, n, levels);
+    h->lv.resize(ns.size());
+    size_t maxndof = 0;
+    for (size_t l = 0; l < ns.size(); ++l) {
+      Level& L = h->lv[l];
+      L.n = ns[l];
+      L.m = ns[l] + p - 2;
+      L.nscal = 1;
+      for (int a = 0; a < dim; ++a) L.nscal *= (size_t)L.m;
+      L.ndof = dim * L.nscal;
+      maxndof = std::max(maxndof, L.ndof);
+      assemble_level(*h, L, s);
+      IGACD_CUDA(cudaMalloc(&L.b, sizeof(double) * L.ndof));
+      IGACD_CUDA(cudaMalloc(&L.x, sizeof(double) * L.ndof));
+      IGACD_CUDA(cudaMalloc(&L.t, sizeof(double) * L.ndof));
+      IGACD_CUDA(cudaMalloc(&L.r, sizeof(double) * L.ndof));
+    }
+    h->tr.resize(ns.size() - 1);
+    size_t scratch = 1;
+    for (size_t l = 0; l + 1 < ns.size(); ++l) {
+      build_transfer(*h, p, ns[l + 1], h->tr[l], s);
+      const size_t mf = h->tr[l].mf, mc = h->tr[l].mc;
+      scratch = std::max(scratch, dim == 2 ? (size_t)dim * mc * mf : (size_t)dim * mc * mf * mf);
+    }
+    h->scratch_len = scratch;
+    IGACD_CUDA(cudaMalloc(&h->scratch0, sizeof(double) * scratch));
+    IGACD_CUDA(cudaMalloc(&h->scratch1, sizeof(double) * scratch));
+    size_t np = 1;
+    for (size_t l = 0; l < ns.size(); ++l) {
+      np = std::max(np, (size_t)operator_ctas(*h, (int)l));
+      np = std::max(np, (size_t)vec_ctas(h->lv[l].ndof));
+    }
+    h->partial_len = np;
+    IGACD_CUDA(cudaMalloc(&h->partial, sizeof(double) * np));
+    IGACD_CUDA(cudaMalloc(&h->scal, sizeof(double) * NSLOT));
+    IGACD_CUDA(cudaMallocHost(&h->hscal, sizeof(double) * NSLOT));
+    const size_t n0 = h->lv[0].ndof;
+    IGACD_CUDA(cudaMalloc(&h->pr, sizeof(double) * n0));
+    IGACD_CUDA(cudaMalloc(&h->pz, sizeof(double) * n0));
+    IGACD_CUDA(cudaMalloc(&h->pp, sizeof(double) * n0));
+    IGACD_CUDA(cudaMalloc(&h->pq, sizeof(double) * n0));
+    // the dense coarse inverse is built only when the coarsest level is small enough;
+    // otherwise the handle still applies the operator but refuses V-cycles / solves
+    if (h->lv.back().ndof <= COARSE_DENSE_MAX) build_coarse_inverse(*h, s);
+    for (size_t l = 0; l + 1 < ns.size(); ++l) estimate_omega(*h, (int)l, s);
+    IGACD_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    destroy_handle(h);
+    throw;
+  }
+  return h;
+}
+
+// ---- V-cycle ------------------------------------------------------------------------------
+static void jacobi_sweeps(Handle& h, int l, const double* b, double*& cur, double*& oth, int sweeps, double omega,
+                          cudaStream_t s) {
+  Epi ep{};
+  ep.omega = omega;
+  ep.b = b;
+  for (int k = 0; k < sweeps; ++k) {
+    launch_operator(h, l, cur, oth, EPI_JACOBI, DOT_NONE, ep, s);
+    std::swap(cur, oth);
+  }
+}
+
+// x = V_l b from a zero initial guess (pre-smooth, residual,
+// restrict, recurse, prolongate-and-correct, post-smooth).  The result lands in x.
+static void vcycle_level(Handle& h, int l, const double* b, double* x, cudaStream_t s) {
+  const int Lc = (int)h.lv.size() - 1;
+  if (!h.cinv)
+    throw Error{IGACD_E_ARG, "coarsest level too large for the dense coarse solver (" +
+                                 std::to_string(h.lv.back().ndof) + " dofs); choose n divisible by a higher power of 2"};
+  if (l == Lc) {
+    launch_coarse_solve(h, b, x, s);
+    return;
+  }
+  Level& L = h.lv[l];
+  const int swaps = std::max(0, h.nu_pre - 1) + h.nu_post;
+  double* cur = (swaps % 2 == 0) ? x : L.t;
+  double* oth = (cur == x) ? L.t : x;
+  if (h.nu_pre >= 1) {
+    launch_scale_dinv(h, l, b, cur, L.omega, s);   // first sweep from x = 0: x = omega D^-1 b
+    jacobi_sweeps(h, l, b, cur, oth, h.nu_pre - 1, L.omega, s);
+  } else {
+    launch_zero(h, cur, L.ndof, s);
+  }
+  Epi ep{};
+  ep.b = b;
+  launch_operator(h, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
+  Level& C = h.lv[l + 1];
+  launch_restrict(h, l, L.r, C.b, s);
+  vcycle_level(h, l + 1, C.b, C.x, s);
+  launch_prolong(h, l, C.x, cur, true, s);
+  jacobi_sweeps(h, l, b, cur, oth, h.nu_post, L.omega, s);
+  if (cur != x) launch_copy(h, cur, x, L.ndof, s);
+}
+
+// ---- PCG ---------------------------------------------------------------------------------
+static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
+               cudaStream_t s) {
+  const size_t N = h.lv[0].ndof;
+  const int nv = vec_ctas(N);
+  launch_copy(h, b, h.pr, N, s);
+  launch_dot(h, h.pr, h.pr, N, h.partial, s);
+  const double rr0 = reduce_to_host(h, nv, S_RR, s);
+  launch_zero(h, x, N, s);
+  const double r0 = std::sqrt(rr0);
+  if (iters) *iters = 0;
+  if (relres) *relres = 0.0;
+  if (r0 == 0.0) return IGACD_OK;
+  vcycle_level(h, 0, h.pr, h.pz, s);
+  launch_dot(h, h.pr, h.pz, N, h.partial, s);
+  int rz = S_RZ0;
+  launch_finalize(h, h.partial, nv, h.scal + rz, s);
+  launch_copy(h, h.pz, h.pp, N, s);
+  Epi ep{};
+  ep.partial = h.partial;
+  double rel = 1.0;
+  int it = 0;
+  for (it = 1; it <= maxit; ++it) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h.profiling) {
+      IGACD_CUDA(cudaEventCreate(&e0));
+      IGACD_CUDA(cudaEventCreate(&e1));
+      IGACD_CUDA(cudaEventRecord(e0, s));
+    }
+    const int np = launch_operator(h, 0, h.pp, h.pq, EPI_APPLY, DOT_X_OUT, ep, s);
+    h.apply_launches++;
+    if (h.profiling) {
+      IGACD_CUDA(cudaEventRecord(e1, s));
+      h.ev_pending.push_back({e0, e1});
+    }
+    launch_finalize(h, h.partial, np, h.scal + S_PQ, s);
+    launch_pcg_update_xr(h, x, h.pr, h.pp, h.pq, N, h.scal + rz, h.scal + S_PQ, h.partial, s);
+    const double rr = reduce_to_host(h, nv, S_RR, s);
+    rel = std::sqrt(rr) / r0;
+    if (rel < tol) break;
+    if (it == maxit) break;
+    vcycle_level(h, 0, h.pr, h.pz, s);
+    launch_dot(h, h.pr, h.pz, N, h.partial, s);
+    const int rzn = rz == S_RZ0 ? S_RZ1 : S_RZ0;
+    launch_finalize(h, h.partial, nv, h.scal + rzn, s);
+    launch_pcg_update_p(h, h.pp, h.pz, N, h.scal + rzn, h.scal + rz, s);
+    rz = rzn;
+  }
+  if (h.profiling) {
+    IGACD_CUDA(cudaStreamSynchronize(s));
+    for (auto& pr : h.ev_pending) {
+      float ms = 0.f;
+      IGACD_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      h.apply_ms += ms;
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    h.ev_pending.clear();
+  }
+  if (iters) *iters = std::min(it, maxit);
+  if (relres) *relres = rel;
+  return rel < tol ? IGACD_OK : IGACD_E_NOCONV;
+}
+
+}  // namespace igacd
+
+using namespace igacd;
+
+#define API_BEGIN try {
+#define API_END                          \
+  }                                      \
+  catch (const Error& e) {               \
+    set_error(e.msg);                    \
+    return e.code;                       \
+  }                                      \
+  catch (const std::exception& e) {      \
+    set_error(e.what());                 \
+    return IGACD_E_CUDA;                 \
+  }                                      \
+  return IGACD_OK;
+
+static Handle* H(igacd_handle h) {
+  if (!h) throw Error{IGACD_E_ARG, "null handle"};
+  return reinterpret_cast<Handle*>(h);
+}
+static void check_level(Handle* h, int level, bool need_coarser = false) {
+  if (level < 0 || level >= (int)h->lv.size() || (need_coarser && level + 1 >= (int)h->lv.size()))
+    throw Error{IGACD_E_ARG, "level out of range"};
+}
+static void check_ptr(const void* p) {
+  if (!p) throw Error{IGACD_E_ARG, "null pointer argument"};
+}
+
+extern "C" {
+
+int igacd_create(igacd_handle* out, int dim, int p, int n, double nu, double beta, double lambda, const double* b0,
+                 int levels, int nu_pre, int nu_post, void* stream) {
+  API_BEGIN
+  check_ptr(out);
+  *out = nullptr;
+  check_ptr(b0);
+  if (dim != 2 && dim != 3) throw Error{IGACD_E_ARG, "dim must be 2 or 3"};
+  if (!(nu >= 0 && beta >= 0 && lambda >= 0)) throw Error{IGACD_E_ARG, "nu, beta, lambda must be >= 0"};
+  double mass[9], K[81];
+  alfven_form(dim, nu, beta, lambda, b0, mass, K);
+  *out = reinterpret_cast<igacd_handle>(create_impl(dim, p, n, mass, K, levels, nu_pre, nu_post, (cudaStream_t)stream));
+  API_END
+}
+
+int igacd_create_form(igacd_handle* out, int dim, int p, int n, const double* mass, const double* K, int levels,
+                      int nu_pre, int nu_post, void* stream) {
+  API_BEGIN
+  check_ptr(out);
+  *out = nullptr;
+  check_ptr(mass);
+  check_ptr(K);
+  *out = reinterpret_cast<igacd_handle>(create_impl(dim, p, n, mass, K, levels, nu_pre, nu_post, (cudaStream_t)stream));
+  API_END
+}
+
+int igacd_destroy(igacd_handle h) {
+  API_BEGIN
+  if (h) {
+    cudaDeviceSynchronize();
+    destroy_handle(reinterpret_cast<Handle*>(h));
+  }
+  API_END
+}
+
+int igacd_get_info(igacd_handle h, int* dim, int* p, int* levels) {
+  API_BEGIN
+  Handle* hh = H(h);
+  if (dim) *dim = hh->dim;
+  if (p) *p = hh->p;
+  if (levels) *levels = (int)hh->lv.size();
+  API_END
+}
+
+int igacd_num_levels(igacd_handle h, int* levels) {
+  API_BEGIN
+  check_ptr(levels);
+  *levels = (int)H(h)->lv.size();
+  API_END
+}
+
+int igacd_level_n(igacd_handle h, int level, int* n) {
+  API_BEGIN
+  check_ptr(n);
+  check_level(H(h), level);
+  *n = H(h)->lv[level].n;
+  API_END
+}
+
+int igacd_ndof(igacd_handle h, int level, size_t* ndof) {
+  API_BEGIN
+  check_ptr(ndof);
+  check_level(H(h), level);
+  *ndof = H(h)->lv[level].ndof;
+  API_END
+}
+
+int igacd_smoother_omega(igacd_handle h, int level, double* omega, double* rho) {
+  API_BEGIN
+  check_level(H(h), level);
+  if (omega) *omega = H(h)->lv[level].omega;
+  if (rho) *rho = H(h)->lv[level].rho;
+  API_END
+}
+
+int igacd_apply(igacd_handle h, int level, const double* x, double* y, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level);
+  check_ptr(x);
+  check_ptr(y);
+  if (x == y) throw Error{IGACD_E_ARG, "x and y must not alias"};
+  Epi ep{};
+  launch_operator(*hh, level, x, y, EPI_APPLY, DOT_NONE, ep, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_residual(igacd_handle h, int level, const double* b, const double* x, double* r, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level);
+  check_ptr(b);
+  check_ptr(x);
+  check_ptr(r);
+  if (r == x || r == b) throw Error{IGACD_E_ARG, "r must not alias b or x"};
+  Epi ep{};
+  ep.b = b;
+  launch_operator(*hh, level, x, r, EPI_RESID, DOT_NONE, ep, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_smooth(igacd_handle h, int level, const double* b, double* x, int sweeps, double omega, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level);
+  check_ptr(b);
+  check_ptr(x);
+  if (sweeps < 0) throw Error{IGACD_E_ARG, "negative sweeps"};
+  Level& L = hh->lv[level];
+  const double w = omega > 0 ? omega : L.omega;
+  if (!(w > 0)) throw Error{IGACD_E_ARG, "no smoother parameter on this level; pass omega > 0"};
+  double* cur = x;
+  double* oth = L.t;
+  jacobi_sweeps(*hh, level, b, cur, oth, sweeps, w, (cudaStream_t)stream);
+  if (cur != x) launch_copy(*hh, cur, x, L.ndof, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_restrict(igacd_handle h, int level, const double* x_fine, double* x_coarse, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level, true);
+  check_ptr(x_fine);
+  check_ptr(x_coarse);
+  launch_restrict(*hh, level, x_fine, x_coarse, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_prolong(igacd_handle h, int level, const double* x_coarse, double* x_fine, int accumulate, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level, true);
+  check_ptr(x_fine);
+  check_ptr(x_coarse);
+  launch_prolong(*hh, level, x_coarse, x_fine, accumulate != 0, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_vcycle(igacd_handle h, const double* b, double* x, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_ptr(b);
+  check_ptr(x);
+  if (b == x) throw Error{IGACD_E_ARG, "b and x must not alias"};
+  vcycle_level(*hh, 0, b, x, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_solve(igacd_handle h, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
+                void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_ptr(b);
+  check_ptr(x);
+  if (b == x) throw Error{IGACD_E_ARG, "b and x must not alias"};
+  if (!(tol > 0) || maxit < 1) throw Error{IGACD_E_ARG, "need tol > 0 and maxit >= 1"};
+  const int rc = pcg(*hh, b, x, tol, maxit, iters, relres, (cudaStream_t)stream);
+  if (rc != IGACD_OK) {
+    set_error("PCG reached maxit without the requested relative residual");
+    return rc;
+  }
+  API_END
+}
+
+int igacd_solve_host(igacd_handle h, const double* b_host, double* x_host, double tol, int maxit, int* iters,
+                     double* relres, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_ptr(b_host);
+  check_ptr(x_host);
+  if (!(tol > 0) || maxit < 1) throw Error{IGACD_E_ARG, "need tol > 0 and maxit >= 1"};
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t N = hh->lv[0].ndof;
+  if (!hh->px) IGACD_CUDA(cudaMalloc(&hh->px, sizeof(double) * N));
+  if (!hh->pb) IGACD_CUDA(cudaMalloc(&hh->pb, sizeof(double) * N));
+  IGACD_CUDA(cudaMemcpyAsync(hh->pb, b_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  const int rc = pcg(*hh, hh->pb, hh->px, tol, maxit, iters, relres, s);
+  IGACD_CUDA(cudaMemcpyAsync(x_host, hh->px, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+  IGACD_CUDA(cudaStreamSynchronize(s));
+  if (rc != IGACD_OK) {
+    set_error("PCG reached maxit without the requested relative residual");
+    return rc;
+  }
+  API_END
+}
+
+int igacd_get_band(igacd_handle h, int level, int which, double* band_host) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level);
+  check_ptr(band_host);
+  if (which < 0 || which > 2) throw Error{IGACD_E_ARG, "which must be 0 (M), 1 (A) or 2 (S)"};
+  const auto& v = hh->lv[level].hband[which];
+  std::memcpy(band_host, v.data(), sizeof(double) * v.size());
+  API_END
+}
+
+int igacd_get_prolongation(igacd_handle h, int level, double* P_host) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level, true);
+  check_ptr(P_host);
+  const auto& v = hh->tr[level].hdense;
+  std::memcpy(P_host, v.data(), sizeof(double) * v.size());
+  API_END
+}
+
+int igacd_set_profiling(igacd_handle h, int enable) {
+  API_BEGIN
+  H(h)->profiling = enable != 0;
+  API_END
+}
+
+int igacd_get_profile(igacd_handle h, long long* launches, long long* apply_launches, double* apply_ms) {
+  API_BEGIN
+  Handle* hh = H(h);
+  if (launches) *launches = hh->launches;
+  if (apply_launches) *apply_launches = hh->apply_launches;
+  if (apply_ms) *apply_ms = hh->apply_ms;
+  API_END
+}
+
+int igacd_reset_profile(igacd_handle h) {
+  API_BEGIN
+  Handle* hh = H(h);
+  hh->launches = 0;
+  hh->apply_launches = 0;
+  hh->apply_ms = 0.0;
+  API_END
+}
+
+const char* igacd_last_error(void) { return g_last_error.c_str(); }
+const char* igacd_version(void) { return "igacd 0.1 (sm_100a)"; }
+
+}  // extern "C"

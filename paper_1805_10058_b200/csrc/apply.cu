@@ -1,0 +1,519 @@
+// R2: matrix-free operator y = A x by sum factorisation, fused epilogues (R4 smoother,
+// residual, D^-1 A, dot products).
+//
+// The Galerkin matrix is sum_P C_P (x) F_P with 1D factors M, A, S in every direction
+// (eq:matr_Amu PAPER.md:483-492, eq:matr_Amu3D PAPER.md:515-543; the L_A form of reading
+// R1 has the same Kronecker patterns, see internal.cuh Coef).  Each kernel streams the
+// slowest direction ("2.5D marching"): for every slab s it contracts the in-slab
+// directions from shared memory, forms the per-point combinations z_{i,F0}(s), and
+// scatters F0[t][s] z(s) into a register ring of 2p+1 output slabs; slab t = s-p is then
+// final and leaves through the epilogue.  Interior rows of every 1D factor are Toeplitz
+// (PAPER.md:347-354): in-slab contractions use 2p+1 register weights with symmetric
+// pairing (one add feeds M and S, one subtract feeds A); threads whose row lies in the
+// boundary zone redo their contraction with the row's own band.
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace igacd {
+
+// ---------------------------------------------------------------------------------------
+// 2D
+// ---------------------------------------------------------------------------------------
+template <int P, int NT>
+__global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, int mode, int dot,
+                                             const double* __restrict__ x, double* __restrict__ y,
+                                             int chunk) {
+  constexpr int R = 2 * P + 1;
+  constexpr int W = NT + 2 * P;
+  constexpr int LPT = (W + NT - 1) / NT;
+  __shared__ double xs[2][2][W];
+  __shared__ double red[NT / 32];
+  const int m = op.m;
+  const size_t ms = (size_t)m * m;
+  const int tid = threadIdx.x;
+  const int t0 = blockIdx.x * NT;
+  const int k = t0 + tid;
+  const bool active = k < m;
+  const int c0 = blockIdx.y * chunk;
+  const int c1 = min(c0 + chunk, m);
+  const int sb = max(0, c0 - P);
+  const int se = c1 + P;
+  const bool zone = active && (k < op.zoneL || k >= op.zoneR);
+
+  double acc0[R], acc1[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc0[r] = acc1[r] = 0.0;
+  double dsum = 0.0;
+  double pre[2][LPT];
+
+  auto gload = [&](int s) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int i = 0; i < LPT; ++i) {
+        const int idx = tid + i * NT;
+        const int col = t0 - P + idx;
+        double v = 0.0;
+        if (idx < W && s < m && col >= 0 && col < m) v = __ldg(x + j * ms + (size_t)s * m + col);
+        pre[j][i] = v;
+      }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int i = 0; i < LPT; ++i) {
+        const int idx = tid + i * NT;
+        if (idx < W) xs[buf][j][idx] = pre[j][i];
+      }
+  };
+
+  gload(sb);
+  sstore(0);
+  __syncthreads();
+  for (int g = sb; g < se; g += R) {
+#pragma unroll
+    for (int ph = 0; ph < R; ++ph) {
+      const int s = g + ph;
+      if (s < se) {
+        const int buf = (s - sb) & 1;
+        const bool more = s + 1 < se;
+        if (more) gload(s + 1);
+        if (s < m) {
+          double zM[2], zS[2], zA[2];
+          {
+            double uM[2], uS[2], uA[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const double* xr = &xs[buf][j][tid + P];
+              const double xc = xr[0];
+              double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
+#pragma unroll
+              for (int o = 1; o <= P; ++o) {
+                const double lo = xr[-o], hi = xr[o];
+                const double sp = lo + hi, sm = hi - lo;
+                vm = fma(op.tM[o], sp, vm);
+                vs = fma(op.tS[o], sp, vs);
+                va = fma(op.tA[o], sm, va);
+              }
+              if (zone) {
+                const double* rM = op.bM + (size_t)k * R + P;
+                const double* rS = op.bS + (size_t)k * R + P;
+                const double* rA = op.bA + (size_t)k * R + P;
+                vm = vs = va = 0.0;
+#pragma unroll
+                for (int o = -P; o <= P; ++o) {
+                  const double v = xr[o];
+                  vm = fma(__ldg(rM + o), v, vm);
+                  vs = fma(__ldg(rS + o), v, vs);
+                  va = fma(__ldg(rA + o), v, va);
+                }
+              }
+              uM[j] = vm;
+              uS[j] = vs;
+              uA[j] = va;
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              zM[i] = op.c.mass[i][0] * uM[0] + op.c.mass[i][1] * uM[1] + op.c.S[1][i][0] * uS[0] +
+                      op.c.S[1][i][1] * uS[1];
+              zS[i] = op.c.S[0][i][0] * uM[0] + op.c.S[0][i][1] * uM[1];
+              zA[i] = op.c.AA[0][i][0] * uA[0] + op.c.AA[0][i][1] * uA[1];
+            }
+          }
+#pragma unroll
+          for (int o = -P; o <= P; ++o) {
+            const int t = s + o;
+            if (t >= c0 && t < c1) {
+              const size_t wi = (size_t)t * R + P - o;   // F[t][s], s - t = -o
+              const double wM = __ldg(op.bM + wi), wS = __ldg(op.bS + wi), wA = __ldg(op.bA + wi);
+              const int slot = (ph + o + R) % R;
+              acc0[slot] = fma(wM, zM[0], fma(wS, zS[0], fma(wA, zA[0], acc0[slot])));
+              acc1[slot] = fma(wM, zM[1], fma(wS, zS[1], fma(wA, zA[1], acc1[slot])));
+            }
+          }
+        }
+        {
+          const int t = s - P;
+          const int slot = (ph + R - P) % R;
+          if (t >= c0 && t < c1 && active) {
+            const size_t pt = (size_t)t * m + k;
+            double D0 = 1.0, D1 = 1.0;
+            if (mode >= EPI_JACOBI) {
+              const double Mt = __ldg(op.bM + (size_t)t * R + P), St = __ldg(op.bS + (size_t)t * R + P);
+              const double Mk = __ldg(op.bM + (size_t)k * R + P), Sk = __ldg(op.bS + (size_t)k * R + P);
+              D0 = op.c.mass[0][0] * Mt * Mk + op.c.S[0][0][0] * St * Mk + op.c.S[1][0][0] * Mt * Sk;
+              D1 = op.c.mass[1][1] * Mt * Mk + op.c.S[0][1][1] * St * Mk + op.c.S[1][1][1] * Mt * Sk;
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const double a = i == 0 ? acc0[slot] : acc1[slot];
+              const double D = i == 0 ? D0 : D1;
+              const size_t gi = (size_t)i * ms + pt;
+              double out;
+              if (mode == EPI_APPLY) out = a;
+              else if (mode == EPI_RESID) out = ep.b[gi] - a;
+              else if (mode == EPI_JACOBI) out = x[gi] + ep.omega * (ep.b[gi] - a) / D;
+              else out = a / D;
+              y[gi] = out;
+              if (dot == DOT_X_OUT) dsum = fma(x[gi], out, dsum);
+              else if (dot == DOT_OUT_OUT) dsum = fma(out, out, dsum);
+            }
+          }
+          acc0[slot] = 0.0;
+          acc1[slot] = 0.0;
+        }
+        if (more) sstore(buf ^ 1);
+        __syncthreads();
+      }
+    }
+  }
+  if (dot != DOT_NONE) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, off);
+    if ((tid & 31) == 0) red[tid >> 5] = dsum;
+    __syncthreads();
+    if (tid == 0) {
+      double sacc = 0.0;
+      for (int w = 0; w < NT / 32; ++w) sacc += red[w];
+      ep.partial[blockIdx.y * gridDim.x + blockIdx.x] = sacc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// 3D
+// ---------------------------------------------------------------------------------------
+template <int P, int T2, int T3>
+struct Op3dShape {
+  static constexpr int NT = T2 * T3;
+  static constexpr int R = 2 * P + 1;
+  static constexpr int HR = T2 + 2 * P;
+  static constexpr int HC = T3 + 2 * P;
+  static constexpr int XS = HR * HC;        // one component of one slab tile
+  static constexpr int US = T2 * HC;        // one stage-A output array
+  static constexpr int SMEM = (2 * 3 * XS + 9 * US) * 8 + (NT / 32) * 8;
+  static constexpr int LPT = (3 * XS + NT - 1) / NT;
+};
+
+template <int P, int T2, int T3>
+__global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep, int mode, int dot,
+                                                 const double* __restrict__ x, double* __restrict__ y,
+                                                 int chunk) {
+  using Sh = Op3dShape<P, T2, T3>;
+  constexpr int NT = Sh::NT, R = Sh::R, HR = Sh::HR, HC = Sh::HC, XS = Sh::XS, US = Sh::US, LPT = Sh::LPT;
+  extern __shared__ double smem[];
+  double* xs = smem;                  // [2][3][HR][HC]
+  double* us = smem + 2 * 3 * XS;     // [9][T2][HC]: index (F*3 + j), F: 0 M, 1 S, 2 A
+  double* red = us + 9 * US;
+  const int m = op.m;
+  const size_t ms = (size_t)m * m;
+  const size_t m3 = ms * m;
+  const int tid = threadIdx.x;
+  const int tr = tid / T3, tc = tid % T3;
+  const int r0 = blockIdx.y * T2, q0 = blockIdx.x * T3;
+  const int gr = r0 + tr, gc = q0 + tc;
+  const bool active = gr < m && gc < m;
+  const bool zoneB = active && (gc < op.zoneL || gc >= op.zoneR);
+  const int c0 = blockIdx.z * chunk;
+  const int c1 = min(c0 + chunk, m);
+  const int sb = max(0, c0 - P);
+  const int se = c1 + P;
+
+  double acc[3][R];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[i][r] = 0.0;
+  double dsum = 0.0;
+  double pre[LPT];
+
+  auto gload = [&](int s) {
+#pragma unroll
+    for (int i = 0; i < LPT; ++i) {
+      const int idx = tid + i * NT;
+      double v = 0.0;
+      if (idx < 3 * XS && s < m) {
+        const int j = idx / XS, rem = idx % XS;
+        const int hr = rem / HC, hc = rem % HC;
+        const int g1 = r0 - P + hr, g2 = q0 - P + hc;
+        if (g1 >= 0 && g1 < m && g2 >= 0 && g2 < m) v = __ldg(x + j * m3 + (size_t)s * ms + (size_t)g1 * m + g2);
+      }
+      pre[i] = v;
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < LPT; ++i) {
+      const int idx = tid + i * NT;
+      if (idx < 3 * XS) xs[buf * 3 * XS + idx] = pre[i];
+    }
+  };
+
+  gload(sb);
+  sstore(0);
+  __syncthreads();
+  for (int g = sb; g < se; g += R) {
+#pragma unroll
+    for (int ph = 0; ph < R; ++ph) {
+      const int s = g + ph;
+      if (s < se) {
+        const int buf = (s - sb) & 1;
+        const bool more = s + 1 < se;
+        if (more) gload(s + 1);
+        if (s < m) {
+          // ---- stage A: contract direction 1 for rows [0,T2) x halo columns [0,HC)
+          for (int it = tid; it < T2 * HC; it += NT) {
+            const int r = it / HC, cc = it % HC;
+            const int g1 = r0 + r;
+            const bool zoneA = g1 < m && (g1 < op.zoneL || g1 >= op.zoneR);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const double* xc_ = xs + buf * 3 * XS + j * XS + (r + P) * HC + cc;
+              const double xc = xc_[0];
+              double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
+#pragma unroll
+              for (int o = 1; o <= P; ++o) {
+                const double lo = xc_[-o * HC], hi = xc_[o * HC];
+                const double sp = lo + hi, sm = hi - lo;
+                vm = fma(op.tM[o], sp, vm);
+                vs = fma(op.tS[o], sp, vs);
+                va = fma(op.tA[o], sm, va);
+              }
+              if (zoneA) {
+                const double* rM = op.bM + (size_t)g1 * R + P;
+                const double* rS = op.bS + (size_t)g1 * R + P;
+                const double* rA = op.bA + (size_t)g1 * R + P;
+                vm = vs = va = 0.0;
+#pragma unroll
+                for (int o = -P; o <= P; ++o) {
+                  const double v = xc_[o * HC];
+                  vm = fma(__ldg(rM + o), v, vm);
+                  vs = fma(__ldg(rS + o), v, vs);
+                  va = fma(__ldg(rA + o), v, va);
+                }
+              }
+              us[(0 * 3 + j) * US + it] = vm;
+              us[(1 * 3 + j) * US + it] = vs;
+              us[(2 * 3 + j) * US + it] = va;
+            }
+          }
+          __syncthreads();
+          // ---- stage B: contract direction 2, combine patterns into z_{i,F0}
+          double zM[3] = {0, 0, 0}, zS[3] = {0, 0, 0}, zA[3] = {0, 0, 0};
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const double* uM = us + (0 * 3 + j) * US + tr * HC + tc + P;
+            const double* uS = us + (1 * 3 + j) * US + tr * HC + tc + P;
+            const double* uA = us + (2 * 3 + j) * US + tr * HC + tc + P;
+            double vMM, vMS, vMA, vSM, vAM, vAA;
+            {
+              const double c = uM[0];
+              double a1 = op.tM[0] * c, a2 = op.tS[0] * c, a3 = 0.0;
+#pragma unroll
+              for (int o = 1; o <= P; ++o) {
+                const double lo = uM[-o], hi = uM[o];
+                const double sp = lo + hi, sm = hi - lo;
+                a1 = fma(op.tM[o], sp, a1);
+                a2 = fma(op.tS[o], sp, a2);
+                a3 = fma(op.tA[o], sm, a3);
+              }
+              vMM = a1; vMS = a2; vMA = a3;
+            }
+            {
+              double a1 = op.tM[0] * uS[0];
+#pragma unroll
+              for (int o = 1; o <= P; ++o) a1 = fma(op.tM[o], uS[-o] + uS[o], a1);
+              vSM = a1;
+            }
+            {
+              const double c = uA[0];
+              double a1 = op.tM[0] * c, a3 = 0.0;
+#pragma unroll
+              for (int o = 1; o <= P; ++o) {
+                const double lo = uA[-o], hi = uA[o];
+                a1 = fma(op.tM[o], lo + hi, a1);
+                a3 = fma(op.tA[o], hi - lo, a3);
+              }
+              vAM = a1; vAA = a3;
+            }
+            if (zoneB) {
+              const double* rM = op.bM + (size_t)gc * R + P;
+              const double* rS = op.bS + (size_t)gc * R + P;
+              const double* rA = op.bA + (size_t)gc * R + P;
+              vMM = vMS = vMA = vSM = vAM = vAA = 0.0;
+#pragma unroll
+              for (int o = -P; o <= P; ++o) {
+                const double wm = __ldg(rM + o), ws = __ldg(rS + o), wa = __ldg(rA + o);
+                vMM = fma(wm, uM[o], vMM);
+                vMS = fma(ws, uM[o], vMS);
+                vMA = fma(wa, uM[o], vMA);
+                vSM = fma(wm, uS[o], vSM);
+                vAM = fma(wm, uA[o], vAM);
+                vAA = fma(wa, uA[o], vAA);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              zM[i] = fma(op.c.mass[i][j], vMM, zM[i]);
+              zS[i] = fma(op.c.S[0][i][j], vMM, zS[i]);
+              zM[i] = fma(op.c.S[1][i][j], vSM, zM[i]);
+              zM[i] = fma(op.c.S[2][i][j], vMS, zM[i]);
+              zA[i] = fma(op.c.AA[0][i][j], vAM, zA[i]);
+              zA[i] = fma(op.c.AA[1][i][j], vMA, zA[i]);
+              zM[i] = fma(op.c.AA[2][i][j], vAA, zM[i]);
+            }
+          }
+          // ---- stage C: scatter along direction 0 into the ring
+#pragma unroll
+          for (int o = -P; o <= P; ++o) {
+            const int t = s + o;
+            if (t >= c0 && t < c1) {
+              const size_t wi = (size_t)t * R + P - o;
+              const double wM = __ldg(op.bM + wi), wS = __ldg(op.bS + wi), wA = __ldg(op.bA + wi);
+              const int slot = (ph + o + R) % R;
+#pragma unroll
+              for (int i = 0; i < 3; ++i) acc[i][slot] = fma(wM, zM[i], fma(wS, zS[i], fma(wA, zA[i], acc[i][slot])));
+            }
+          }
+        }
+        {
+          const int t = s - P;
+          const int slot = (ph + R - P) % R;
+          if (t >= c0 && t < c1 && active) {
+            const size_t pt = (size_t)t * ms + (size_t)gr * m + gc;
+            double Dv[3] = {1.0, 1.0, 1.0};
+            if (mode >= EPI_JACOBI) {
+              const double M0 = __ldg(op.bM + (size_t)t * R + P), S0 = __ldg(op.bS + (size_t)t * R + P);
+              const double M1 = __ldg(op.bM + (size_t)gr * R + P), S1 = __ldg(op.bS + (size_t)gr * R + P);
+              const double M2 = __ldg(op.bM + (size_t)gc * R + P), S2 = __ldg(op.bS + (size_t)gc * R + P);
+#pragma unroll
+              for (int i = 0; i < 3; ++i)
+                Dv[i] = op.c.mass[i][i] * M0 * M1 * M2 + op.c.S[0][i][i] * S0 * M1 * M2 +
+                        op.c.S[1][i][i] * M0 * S1 * M2 + op.c.S[2][i][i] * M0 * M1 * S2;
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              const double a = acc[i][slot];
+              const size_t gi = (size_t)i * m3 + pt;
+              double out;
+              if (mode == EPI_APPLY) out = a;
+              else if (mode == EPI_RESID) out = ep.b[gi] - a;
+              else if (mode == EPI_JACOBI) out = x[gi] + ep.omega * (ep.b[gi] - a) / Dv[i];
+              else out = a / Dv[i];
+              y[gi] = out;
+              if (dot == DOT_X_OUT) dsum = fma(x[gi], out, dsum);
+              else if (dot == DOT_OUT_OUT) dsum = fma(out, out, dsum);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 3; ++i) acc[i][slot] = 0.0;
+        }
+        if (more) sstore(buf ^ 1);
+        __syncthreads();
+      }
+    }
+  }
+  if (dot != DOT_NONE) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, off);
+    if ((tid & 31) == 0) red[tid >> 5] = dsum;
+    __syncthreads();
+    if (tid == 0) {
+      double sacc = 0.0;
+      for (int w = 0; w < NT / 32; ++w) sacc += red[w];
+      ep.partial[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = sacc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// launch configuration
+// ---------------------------------------------------------------------------------------
+constexpr int NT2D = 128;
+constexpr int T2_3D = 8, T3_3D = 32;
+constexpr int TARGET_CTAS = 4 * 148;
+
+struct Grid {
+  dim3 grid;
+  int chunk;
+};
+
+static Grid grid_for(const Handle& h, int level) {
+  const int m = h.lv[level].m;
+  Grid g;
+  if (h.dim == 2) {
+    const int tx = (m + NT2D - 1) / NT2D;
+    int nch = std::max(1, std::min(m, (TARGET_CTAS + tx - 1) / tx));
+    g.chunk = (m + nch - 1) / nch;
+    g.chunk = std::max(g.chunk, std::min(m, 4 * h.p));
+    nch = (m + g.chunk - 1) / g.chunk;
+    g.grid = dim3(tx, nch, 1);
+  } else {
+    const int tx = (m + T3_3D - 1) / T3_3D, ty = (m + T2_3D - 1) / T2_3D;
+    int nch = std::max(1, std::min(m, (TARGET_CTAS + tx * ty - 1) / (tx * ty)));
+    g.chunk = (m + nch - 1) / nch;
+    g.chunk = std::max(g.chunk, std::min(m, 4 * h.p));
+    nch = (m + g.chunk - 1) / g.chunk;
+    g.grid = dim3(tx, ty, nch);
+  }
+  return g;
+}
+
+int operator_ctas(const Handle& h, int level) {
+  Grid g = grid_for(h, level);
+  return g.grid.x * g.grid.y * g.grid.z;
+}
+
+template <int P>
+static void launch2d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                     cudaStream_t s) {
+  k_op2d<P, NT2D><<<g.grid, NT2D, 0, s>>>(op, ep, mode, dot, x, y, g.chunk);
+}
+
+template <int P>
+static void launch3d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                     cudaStream_t s) {
+  using Sh = Op3dShape<P, T2_3D, T3_3D>;
+  static bool attr = false;
+  if (!attr) {
+    IGACD_CUDA(cudaFuncSetAttribute(k_op3d<P, T2_3D, T3_3D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM));
+    attr = true;
+  }
+  k_op3d<P, T2_3D, T3_3D><<<g.grid, Sh::NT, Sh::SMEM, s>>>(op, ep, mode, dot, x, y, g.chunk);
+}
+
+int launch_operator(Handle& h, int level, const double* x, double* out, EpiMode mode, DotMode dot, const Epi& epi,
+                    cudaStream_t s) {
+  const Level& L = h.lv[level];
+  Grid g = grid_for(h, level);
+  const int nct = g.grid.x * g.grid.y * g.grid.z;
+  if (dot != DOT_NONE && (size_t)nct > h.partial_len) throw Error{IGACD_E_ARG, "partial buffer too small"};
+  if (h.dim == 2) {
+    switch (h.p) {
+      case 1: launch2d<1>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 2: launch2d<2>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 3: launch2d<3>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 4: launch2d<4>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 5: launch2d<5>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 6: launch2d<6>(g, L.op, epi, mode, dot, x, out, s); break;
+      default: throw Error{IGACD_E_ARG, "degree out of range"};
+    }
+  } else {
+    switch (h.p) {
+      case 1: launch3d<1>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 2: launch3d<2>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 3: launch3d<3>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 4: launch3d<4>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 5: launch3d<5>(g, L.op, epi, mode, dot, x, out, s); break;
+      case 6: launch3d<6>(g, L.op, epi, mode, dot, x, out, s); break;
+      default: throw Error{IGACD_E_ARG, "degree out of range"};
+    }
+  }
+  IGACD_LAUNCH_CHECK();
+  count_launch(h);
+  return dot != DOT_NONE ? nct : 0;
+}
+
+}  // namespace igacd

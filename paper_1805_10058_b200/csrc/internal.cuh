@@ -1,0 +1,156 @@
+// Internal declarations of libigacd (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/igacd.h"
+
+namespace igacd {
+
+constexpr int MAXP = 6;   // highest supported B-spline degree
+constexpr int NCOARSE_MAX = 1500;  // reading R6: coarsen while d*m^d exceeds this
+constexpr int POWER_STEPS = 30;    // reading R4: power steps for rho(D^-1 A)
+constexpr size_t COARSE_DENSE_MAX = 8192;  // largest coarsest level given a dense inverse
+
+// Operator patterns.  With 1D factors
+// M, A (skew), S the Galerkin matrix is
+//   A = sum_ij mass[i][j] M(x)M(x)M  +  sum_l S[l][i][j] (S in direction l, M elsewhere)
+//       + sum_q AA[q][i][j] (A in both directions of pair q, M elsewhere),
+// pairs q: 0 = (0,1), 1 = (0,2), 2 = (1,2); directions 0-based, 0 slowest.
+// (There are no single-A patterns: the forms have no value-derivative products.)
+struct Coef {
+  double mass[3][3];
+  double S[3][3][3];
+  double AA[3][3][3];
+};
+
+// Kernel view of one level's 1D factors (same in every direction: n_1 = .. = n_d = n).
+struct OpParams {
+  int m;             // interior B-splines per direction
+  int zoneL, zoneR;  // rows k < zoneL or k >= zoneR are not Toeplitz (boundary zone)
+  const double* bM;  // band storage [m][2p+1], F[k][k+o] at k*(2p+1)+o+p
+  const double* bA;
+  const double* bS;
+  double tM[MAXP + 1], tA[MAXP + 1], tS[MAXP + 1];  // Toeplitz row F[k][k+o], o = 0..p
+  Coef c;
+};
+
+// Epilogue of the fused operator kernels.
+enum EpiMode { EPI_APPLY = 0, EPI_RESID = 1, EPI_JACOBI = 2, EPI_DINV = 3 };
+enum DotMode { DOT_NONE = 0, DOT_X_OUT = 1, DOT_OUT_OUT = 2 };
+
+struct Epi {
+  double omega;       // EPI_JACOBI
+  const double* b;    // EPI_RESID, EPI_JACOBI
+  double* partial;    // per-CTA partial sums when a DotMode is requested
+};
+
+struct Transfer1D {   // 1D prolongation P (m_f x m_c) in fixed-width row storage
+  int mf = 0, mc = 0;
+  int wp = 0, wr = 0;           // max nonzeros per P row / per P^T row
+  int* p_start = nullptr;       // [mf]  first coarse column of fine row k
+  double* p_w = nullptr;        // [mf][wp]
+  int* r_start = nullptr;       // [mc]  first fine column of coarse row c (row of P^T)
+  double* r_w = nullptr;        // [mc][wr]
+  std::vector<double> hdense;   // host dense copy (debug/parity)
+};
+
+struct Level {
+  int n = 0, m = 0;
+  size_t nscal = 0, ndof = 0;
+  double* band[3] = {nullptr, nullptr, nullptr};  // M, A, S
+  std::vector<double> hband[3];
+  OpParams op;
+  double rho = 0.0, omega = 0.0;
+  // work vectors (ndof each)
+  double* b = nullptr;
+  double* x = nullptr;
+  double* t = nullptr;
+  double* r = nullptr;
+};
+
+struct Handle {
+  int dim = 0, p = 0;
+  int nu_pre = 1, nu_post = 1;
+  Coef coef;
+  std::vector<Level> lv;
+  std::vector<Transfer1D> tr;   // tr[l]: level l+1 -> level l
+  // coarsest level exact inverse (dense, ndof_L x ndof_L)
+  double* cinv = nullptr;
+  // transfer scratch (max size), reductions
+  double* scratch0 = nullptr;
+  double* scratch1 = nullptr;
+  size_t scratch_len = 0;
+  double* partial = nullptr;    // per-CTA partial sums
+  size_t partial_len = 0;
+  double* scal = nullptr;       // device scalars
+  double* hscal = nullptr;      // pinned host mirror
+  // PCG vectors (level-0 size)
+  double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *px = nullptr, *pb = nullptr;
+  cudaStream_t stream = nullptr;
+  // instrumentation
+  long long launches = 0, apply_launches = 0;
+  double apply_ms = 0.0;
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
+};
+
+// ---- error handling ---------------------------------------------------------------
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define IGACD_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::igacd::Error{IGACD_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+#define IGACD_LAUNCH_CHECK() IGACD_CUDA(cudaGetLastError())
+
+// ---- assembly.cu --------------------------------------------------------------------
+void assemble_level(Handle& h, Level& L, cudaStream_t s);
+void build_transfer(Handle& h, int p, int n_coarse, Transfer1D& T, cudaStream_t s);
+void gauss_legendre(int q, double* x01, double* w01);
+
+// ---- apply.cu -----------------------------------------------------------------------
+// out = epilogue(A x); returns number of CTAs that wrote partial sums (0 if dot == DOT_NONE)
+int launch_operator(Handle& h, int level, const double* x, double* out, EpiMode mode, DotMode dot,
+                    const Epi& epi, cudaStream_t s);
+int operator_ctas(const Handle& h, int level);
+
+// ---- transfer.cu --------------------------------------------------------------------
+void launch_prolong(Handle& h, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s);
+void launch_restrict(Handle& h, int level, const double* xf, double* xc, cudaStream_t s);
+
+// ---- coarse.cu ----------------------------------------------------------------------
+void build_coarse_inverse(Handle& h, cudaStream_t s);
+void launch_coarse_solve(Handle& h, const double* b, double* x, cudaStream_t s);
+
+// ---- vec.cu -------------------------------------------------------------------------
+int vec_ctas(size_t n);
+void launch_dot(Handle& h, const double* a, const double* b, size_t n, double* partial, cudaStream_t s);
+void launch_finalize(Handle& h, const double* partial, int nparts, double* dst, cudaStream_t s);
+void launch_scale_dinv(Handle& h, int level, const double* b, double* x, double omega, cudaStream_t s);
+void launch_copy(Handle& h, const double* a, double* b, size_t n, cudaStream_t s);
+void launch_zero(Handle& h, double* a, size_t n, cudaStream_t s);
+void launch_scale(Handle& h, double* a, const double* scal_num, const double* scal_den, size_t n, cudaStream_t s);
+void launch_dvdot(Handle& h, int level, const double* v, double* partial, cudaStream_t s);
+void launch_hash_vector(Handle& h, double* v, size_t n, cudaStream_t s);
+// PCG fused updates (scalars on device: scal[...])
+void launch_pcg_update_xr(Handle& h, double* x, double* r, const double* p, const double* q, size_t n,
+                          const double* rz, const double* pq, double* partial, cudaStream_t s);
+void launch_pcg_update_p(Handle& h, double* p, const double* z, size_t n, const double* rz_new,
+                         const double* rz_old, cudaStream_t s);
+
+// ---- common -------------------------------------------------------------------------
+inline void count_launch(Handle& h) { h.launches++; }
+
+}  // namespace igacd

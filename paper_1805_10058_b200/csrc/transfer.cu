@@ -1,0 +1,73 @@
+// R3: prolongation x_f = (I_d (x) P (x) .. (x) P) x_c and restriction x_c = P^T x_f
+// (eq:2by2prol PAPER.md:1178-1186; R_l := P_l^T), one 1D pass per
+// direction.  Each pass views the array as [outer][axis][inner] and writes one output
+// element per thread from the fixed-width row storage of P (or P^T): coalesced along
+// `inner`, and for the fastest axis consecutive threads read overlapping windows.
+#include "internal.cuh"
+
+namespace igacd {
+
+__global__ void k_axis_pass(const double* __restrict__ in, double* __restrict__ out, long long outer, int nin,
+                            int nout, long long inner, const int* __restrict__ start,
+                            const double* __restrict__ w, int W, int accumulate) {
+  const long long total = outer * nout * inner;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long in_ = idx % inner;
+    const long long t = idx / inner;
+    const int o = (int)(t % nout);
+    const long long ou = t / nout;
+    const int st = __ldg(start + o);
+    const double* src = in + (ou * nin + st) * inner + in_;
+    const double* wr = w + (size_t)o * W;
+    double acc = 0.0;
+    for (int k = 0; k < W; ++k) {
+      if (st + k < nin) acc = fma(__ldg(wr + k), __ldg(src + (long long)k * inner), acc);
+    }
+    if (accumulate) out[idx] += acc;
+    else out[idx] = acc;
+  }
+}
+
+static void axis_pass(Handle& h, const double* in, double* out, long long outer, int nin, int nout, long long inner,
+                      const int* start, const double* w, int W, bool acc, cudaStream_t s) {
+  const long long total = outer * nout * inner;
+  const int bs = 256;
+  long long blocks = (total + bs - 1) / bs;
+  if (blocks > 148LL * 16) blocks = 148LL * 16;
+  if (blocks < 1) blocks = 1;
+  k_axis_pass<<<(unsigned)blocks, bs, 0, s>>>(in, out, outer, nin, nout, inner, start, w, W, acc ? 1 : 0);
+  IGACD_LAUNCH_CHECK();
+  count_launch(h);
+}
+
+// level l (fine, m_f) <- level l+1 (coarse, m_c)
+void launch_prolong(Handle& h, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s) {
+  const Transfer1D& T = h.tr[level];
+  const long long d = h.dim, mf = T.mf, mc = T.mc;
+  if (h.dim == 2) {
+    // [d][mc][mc] -> [d][mc][mf] -> [d][mf][mf]
+    axis_pass(h, xc, h.scratch0, d * mc, (int)mc, (int)mf, 1, T.p_start, T.p_w, T.wp, false, s);
+    axis_pass(h, h.scratch0, xf, d, (int)mc, (int)mf, mf, T.p_start, T.p_w, T.wp, accumulate, s);
+  } else {
+    axis_pass(h, xc, h.scratch0, d * mc * mc, (int)mc, (int)mf, 1, T.p_start, T.p_w, T.wp, false, s);
+    axis_pass(h, h.scratch0, h.scratch1, d * mc, (int)mc, (int)mf, mf, T.p_start, T.p_w, T.wp, false, s);
+    axis_pass(h, h.scratch1, xf, d, (int)mc, (int)mf, mf * mf, T.p_start, T.p_w, T.wp, accumulate, s);
+  }
+}
+
+void launch_restrict(Handle& h, int level, const double* xf, double* xc, cudaStream_t s) {
+  const Transfer1D& T = h.tr[level];
+  const long long d = h.dim, mf = T.mf, mc = T.mc;
+  if (h.dim == 2) {
+    // [d][mf][mf] -> [d][mc][mf] -> [d][mc][mc]
+    axis_pass(h, xf, h.scratch0, d, (int)mf, (int)mc, mf, T.r_start, T.r_w, T.wr, false, s);
+    axis_pass(h, h.scratch0, xc, d * mc, (int)mf, (int)mc, 1, T.r_start, T.r_w, T.wr, false, s);
+  } else {
+    axis_pass(h, xf, h.scratch0, d, (int)mf, (int)mc, mf * mf, T.r_start, T.r_w, T.wr, false, s);
+    axis_pass(h, h.scratch0, h.scratch1, d * mc, (int)mf, (int)mc, mf, T.r_start, T.r_w, T.wr, false, s);
+    axis_pass(h, h.scratch1, xc, d * mc * mc, (int)mf, (int)mc, 1, T.r_start, T.r_w, T.wr, false, s);
+  }
+}
+
+}  // namespace igacd

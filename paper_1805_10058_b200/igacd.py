@@ -1,0 +1,223 @@
+"""Thin ctypes binding of libigacd.so (include/igacd.h).  Argument marshalling only.
+
+Every function has the C name.  Device vectors are torch CUDA float64 tensors (PyTorch is
+used for device memory and streams only); host vectors are numpy float64 arrays or CPU
+tensors.  A nonzero C status raises IgacdError with igacd_last_error().  There is no CPU
+fallback: if the shared library is missing, importing this module raises.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libigacd.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError("libigacd.so not built (%s); run __graft_entry__.build()" % LIB_PATH)
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_c_int, _c_double, _vp, _size_t = ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
+_P = ctypes.POINTER
+
+
+def _sig(name, args):
+    f = getattr(_lib, name)
+    f.restype = _c_int
+    f.argtypes = args
+    return f
+
+
+_lib.igacd_last_error.restype = ctypes.c_char_p
+_lib.igacd_version.restype = ctypes.c_char_p
+_create = _sig("igacd_create", [_P(_vp), _c_int, _c_int, _c_int, _c_double, _c_double, _c_double, _P(_c_double),
+                                _c_int, _c_int, _c_int, _vp])
+_create_form = _sig("igacd_create_form", [_P(_vp), _c_int, _c_int, _c_int, _P(_c_double), _P(_c_double), _c_int,
+                                          _c_int, _c_int, _vp])
+_destroy = _sig("igacd_destroy", [_vp])
+_get_info = _sig("igacd_get_info", [_vp, _P(_c_int), _P(_c_int), _P(_c_int)])
+_num_levels = _sig("igacd_num_levels", [_vp, _P(_c_int)])
+_level_n = _sig("igacd_level_n", [_vp, _c_int, _P(_c_int)])
+_ndof = _sig("igacd_ndof", [_vp, _c_int, _P(_size_t)])
+_omega = _sig("igacd_smoother_omega", [_vp, _c_int, _P(_c_double), _P(_c_double)])
+_apply = _sig("igacd_apply", [_vp, _c_int, _vp, _vp, _vp])
+_residual = _sig("igacd_residual", [_vp, _c_int, _vp, _vp, _vp, _vp])
+_smooth = _sig("igacd_smooth", [_vp, _c_int, _vp, _vp, _c_int, _c_double, _vp])
+_restrict = _sig("igacd_restrict", [_vp, _c_int, _vp, _vp, _vp])
+_prolong = _sig("igacd_prolong", [_vp, _c_int, _vp, _vp, _c_int, _vp])
+_vcycle = _sig("igacd_vcycle", [_vp, _vp, _vp, _vp])
+_solve = _sig("igacd_solve", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
+_solve_host = _sig("igacd_solve_host", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
+_get_band = _sig("igacd_get_band", [_vp, _c_int, _c_int, _P(_c_double)])
+_get_prol = _sig("igacd_get_prolongation", [_vp, _c_int, _P(_c_double)])
+_set_prof = _sig("igacd_set_profiling", [_vp, _c_int])
+_get_prof = _sig("igacd_get_profile", [_vp, _P(ctypes.c_longlong), _P(ctypes.c_longlong), _P(_c_double)])
+_reset_prof = _sig("igacd_reset_profile", [_vp])
+
+IGACD_E_NOCONV = -4
+
+
+class IgacdError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("igacd error %d: %s" % (code, msg))
+        self.code = code
+
+
+def _check(rc):
+    if rc != 0:
+        raise IgacdError(rc, _lib.igacd_last_error().decode())
+
+
+def _dptr(t):
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype.__str__() == "torch.float64" and t.is_contiguous()):
+        raise TypeError("expected a contiguous CUDA float64 tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _darr(vals):
+    a = (_c_double * len(vals))(*[float(v) for v in vals])
+    return a
+
+
+def igacd_version():
+    return _lib.igacd_version().decode()
+
+
+def igacd_create(dim, p, n, nu, beta, lam, b0, levels=0, nu_pre=1, nu_post=1, stream=None):
+    h = _vp()
+    _check(_create(ctypes.byref(h), dim, p, n, nu, beta, lam, _darr(b0), levels, nu_pre, nu_post, _stream(stream)))
+    return h
+
+
+def igacd_create_form(dim, p, n, mass, K, levels=0, nu_pre=1, nu_post=1, stream=None):
+    h = _vp()
+    _check(_create_form(ctypes.byref(h), dim, p, n, _darr(list(mass)), _darr(list(K)), levels, nu_pre, nu_post,
+                        _stream(stream)))
+    return h
+
+
+def igacd_destroy(h):
+    _check(_destroy(h))
+
+
+def igacd_get_info(h):
+    d, p, L = _c_int(), _c_int(), _c_int()
+    _check(_get_info(h, ctypes.byref(d), ctypes.byref(p), ctypes.byref(L)))
+    return d.value, p.value, L.value
+
+
+def igacd_num_levels(h):
+    v = _c_int()
+    _check(_num_levels(h, ctypes.byref(v)))
+    return v.value
+
+
+def igacd_level_n(h, level):
+    v = _c_int()
+    _check(_level_n(h, level, ctypes.byref(v)))
+    return v.value
+
+
+def igacd_ndof(h, level=0):
+    v = _size_t()
+    _check(_ndof(h, level, ctypes.byref(v)))
+    return v.value
+
+
+def igacd_smoother_omega(h, level):
+    w, r = _c_double(), _c_double()
+    _check(_omega(h, level, ctypes.byref(w), ctypes.byref(r)))
+    return w.value, r.value
+
+
+def igacd_apply(h, level, x, y, stream=None):
+    _check(_apply(h, level, _dptr(x), _dptr(y), _stream(stream)))
+
+
+def igacd_residual(h, level, b, x, r, stream=None):
+    _check(_residual(h, level, _dptr(b), _dptr(x), _dptr(r), _stream(stream)))
+
+
+def igacd_smooth(h, level, b, x, sweeps, omega=0.0, stream=None):
+    _check(_smooth(h, level, _dptr(b), _dptr(x), sweeps, omega, _stream(stream)))
+
+
+def igacd_restrict(h, level, x_fine, x_coarse, stream=None):
+    _check(_restrict(h, level, _dptr(x_fine), _dptr(x_coarse), _stream(stream)))
+
+
+def igacd_prolong(h, level, x_coarse, x_fine, accumulate=False, stream=None):
+    _check(_prolong(h, level, _dptr(x_coarse), _dptr(x_fine), 1 if accumulate else 0, _stream(stream)))
+
+
+def igacd_vcycle(h, b, x, stream=None):
+    _check(_vcycle(h, _dptr(b), _dptr(x), _stream(stream)))
+
+
+def igacd_solve(h, b, x, tol, maxit, stream=None, raise_on_noconv=True):
+    it, rel = _c_int(), _c_double()
+    rc = _solve(h, _dptr(b), _dptr(x), tol, maxit, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
+    if rc != IGACD_E_NOCONV or raise_on_noconv:
+        _check(rc)
+    return it.value, rel.value
+
+
+def igacd_solve_host(h, b_host, x_host, tol, maxit, stream=None, raise_on_noconv=True):
+    """b_host / x_host: C-contiguous float64 numpy arrays or CPU tensors (pinned or not)."""
+    def hp(a):
+        if hasattr(a, "data_ptr"):
+            return ctypes.c_void_p(a.data_ptr())
+        return a.ctypes.data_as(ctypes.c_void_p)
+    it, rel = _c_int(), _c_double()
+    rc = _solve_host(h, hp(b_host), hp(x_host), tol, maxit, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
+    if rc != IGACD_E_NOCONV or raise_on_noconv:
+        _check(rc)
+    return it.value, rel.value
+
+
+def igacd_get_band(h, level, which):
+    import numpy as np
+    n = igacd_level_n(h, level)
+    p = _handle_p(h)
+    m = n + p - 2
+    out = np.zeros(m * (2 * p + 1))
+    _check(_get_band(h, level, which, out.ctypes.data_as(_P(_c_double))))
+    return out.reshape(m, 2 * p + 1)
+
+
+def igacd_get_prolongation(h, level):
+    import numpy as np
+    p = _handle_p(h)
+    mf = igacd_level_n(h, level) + p - 2
+    mc = igacd_level_n(h, level + 1) + p - 2
+    out = np.zeros(mf * mc)
+    _check(_get_prol(h, level, out.ctypes.data_as(_P(_c_double))))
+    return out.reshape(mf, mc)
+
+
+def _handle_p(h):
+    return igacd_get_info(h)[1]
+
+
+def igacd_set_profiling(h, enable):
+    _check(_set_prof(h, 1 if enable else 0))
+
+
+def igacd_get_profile(h):
+    a, b, c = ctypes.c_longlong(), ctypes.c_longlong(), _c_double()
+    _check(_get_prof(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return a.value, b.value, c.value
+
+
+def igacd_reset_profile(h):
+    _check(_reset_prof(h))

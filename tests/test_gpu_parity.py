@@ -1,0 +1,310 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, element by element.
+
+Tolerance (north_star): relative error <= 1e-12 on apply, V-cycle, restriction/prolongation;
+solves: same iteration count +-1, requested residual reached, solution difference <= 1e-8.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import inputs
+from oracle import matrices1d as m1
+from oracle.krylov import pcg
+from oracle.multigrid import Hierarchy
+from oracle.operator import Discretization, form_alfven, form_curldiv
+from oracle.transfer import prolongation, prolongation_1d
+
+from .gpu_helpers import assert_close, sample_dofs, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1805_10058_b200 import igacd as ig  # noqa: E402
+
+S2, S3 = 2 ** -0.5, 3 ** -0.5
+PARAMS = dict(nu=0.3, beta=0.05, lam=1.0)
+
+
+def b0_for(d):
+    return (0.6, 0.8) if d == 2 else (0.48, 0.6, 0.64)
+
+
+class Case:
+    def __init__(self, d, p, n, nu=0.3, beta=0.05, lam=1.0, b0=None, levels=0):
+        self.d, self.p, self.n = d, p, n
+        self.nu, self.beta, self.lam = nu, beta, lam
+        self.b0 = b0_for(d) if b0 is None else b0
+        self.levels = levels
+        self.form = form_alfven(nu, beta, lam, self.b0)
+
+    def handle(self, nu_pre=1, nu_post=1):
+        return ig.igacd_create(self.d, self.p, self.n, self.nu, self.beta, self.lam, self.b0,
+                               levels=self.levels, nu_pre=nu_pre, nu_post=nu_post)
+
+    def __repr__(self):
+        return "d%dp%dn%d" % (self.d, self.p, self.n)
+
+
+# sizes span several CTA tiles (2D tile 128 columns, 3D tile 8 x 32) with ragged tails
+APPLY_2D = [Case(2, 1, 140), Case(2, 2, 133), Case(2, 3, 150), Case(2, 4, 129), Case(2, 5, 70), Case(2, 6, 61),
+            Case(2, 3, 3), Case(2, 2, 1)]
+APPLY_3D_FULL = [Case(3, 1, 12), Case(3, 2, 11), Case(3, 3, 7), Case(3, 2, 1), Case(3, 4, 4)]
+APPLY_3D_SAMPLED = [Case(3, 1, 45), Case(3, 2, 41), Case(3, 3, 37), Case(3, 4, 35), Case(3, 5, 30), Case(3, 6, 26)]
+
+
+@pytest.mark.parametrize("case", [Case(2, p, 20) for p in range(1, 7)] + [Case(3, 3, 9), Case(2, 5, 4)], ids=repr)
+def test_bands_match_oracle_1d_matrices(case):
+    h = case.handle()
+    try:
+        M, A, S = m1.matrices(case.p, case.n)
+        m, p = case.n + case.p - 2, case.p
+        for which, F in enumerate([M, A, S]):
+            band = ig.igacd_get_band(h, 0, which)
+            dense = np.zeros((m, m))
+            for k in range(m):
+                for o in range(-p, p + 1):
+                    if 0 <= k + o < m:
+                        dense[k, k + o] = band[k, o + p]
+            assert_close(dense, F, 1e-13, "factor %d" % which)
+    finally:
+        ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("p,nc", [(1, 4), (2, 5), (3, 8), (4, 7), (5, 9), (6, 6), (3, 1), (2, 2)])
+def test_prolongation_matches_oracle(p, nc):
+    h = ig.igacd_create(2, p, 2 * nc, 1.0, 0.1, 1.0, (1.0, 0.0), levels=2)
+    try:
+        assert_close(ig.igacd_get_prolongation(h, 0), prolongation_1d(p, nc), 1e-13, "P")
+    finally:
+        ig.igacd_destroy(h)
+
+
+def _apply_full(case, seed=0):
+    h = case.handle()
+    try:
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        x = np.random.default_rng(seed).uniform(-1, 1, disc.ndof)
+        y = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        ig.igacd_apply(h, 0, to_dev(x), y)
+        return assert_close(to_host(y), A @ x, 1e-12, repr(case))
+    finally:
+        ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("case", APPLY_2D, ids=repr)
+def test_apply_2d_full(case):
+    _apply_full(case)
+
+
+@pytest.mark.parametrize("case", APPLY_3D_FULL, ids=repr)
+def test_apply_3d_full(case):
+    _apply_full(case)
+
+
+@pytest.mark.parametrize("case", APPLY_3D_SAMPLED, ids=repr)
+def test_apply_3d_sampled(case):
+    h = case.handle()
+    try:
+        disc = Discretization(case.d, case.p, case.n)
+        x = np.random.default_rng(1).standard_normal(disc.ndof)
+        y = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        ig.igacd_apply(h, 0, to_dev(x), y)
+        dofs = sample_dofs(3, disc.m, 24)
+        ref = disc.sampled_apply(case.form, x, dofs)
+        yg = to_host(y)
+        # scale: max of the sampled reference rows and of the full GPU vector
+        scale = max(np.max(np.abs(ref)), 1e-300)
+        assert np.max(np.abs(yg[dofs] - ref)) / scale < 1e-12
+    finally:
+        ig.igacd_destroy(h)
+
+
+def test_apply_paper_curldiv_form_2d_3d():
+    # the paper's own operator (eq:curl-div) through igacd_create_form
+    for d, p, n in [(2, 3, 40), (3, 2, 8)]:
+        alpha, beta = 1.0, 0.01
+        K = np.zeros((d, d, d, d))
+        # curl-curl + div-div in (test (i,b), trial (j,a)) form, written out per dimension
+        if d == 2:
+            c = np.zeros((2, 2)); c[1, 0], c[0, 1] = 1.0, -1.0          # curl u = d0 u1 - d1 u0
+            K += alpha * np.einsum("ib,ja->ibja", c, c)
+        else:
+            eps = np.zeros((3, 3, 3))
+            eps[0, 1, 2] = eps[1, 2, 0] = eps[2, 0, 1] = 1
+            eps[0, 2, 1] = eps[2, 1, 0] = eps[1, 0, 2] = -1
+            # (curl u)_k = eps_{k a j} d_a u_j
+            K += alpha * np.einsum("kbi,kaj->ibja", eps, eps)
+        dd = np.eye(d)
+        K += beta * np.einsum("ib,ja->ibja", dd, dd)
+        h = ig.igacd_create_form(d, p, n, np.zeros(d * d), K.ravel(), levels=1)
+        try:
+            disc = Discretization(d, p, n)
+            A = disc.assemble(form_curldiv(alpha, beta))
+            x = np.random.default_rng(7).standard_normal(disc.ndof)
+            y = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+            ig.igacd_apply(h, 0, to_dev(x), y)
+            assert_close(to_host(y), A @ x, 1e-12, "curldiv d=%d" % d)
+        finally:
+            ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("case", [Case(2, 3, 40, levels=3), Case(2, 5, 24, levels=3), Case(3, 2, 8, levels=2),
+                                  Case(3, 4, 8, levels=2)], ids=repr)
+def test_restrict_prolong(case):
+    h = case.handle()
+    try:
+        for lvl in range(case.levels - 1):
+            nf = ig.igacd_level_n(h, lvl)
+            P = prolongation(case.d, case.p, nf // 2)
+            rng = np.random.default_rng(lvl)
+            xf = rng.standard_normal(P.shape[0])
+            xc = rng.standard_normal(P.shape[1])
+            yc = torch.zeros(P.shape[1], dtype=torch.float64, device="cuda")
+            ig.igacd_restrict(h, lvl, to_dev(xf), yc)
+            assert_close(to_host(yc), P.T @ xf, 1e-12, "restrict")
+            yf = to_dev(xf)
+            ig.igacd_prolong(h, lvl, to_dev(xc), yf, accumulate=True)
+            assert_close(to_host(yf), xf + P @ xc, 1e-12, "prolong+")
+            ig.igacd_prolong(h, lvl, to_dev(xc), yf, accumulate=False)
+            assert_close(to_host(yf), P @ xc, 1e-12, "prolong")
+    finally:
+        ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("case", [Case(2, 3, 30, levels=2), Case(3, 3, 6, levels=2)], ids=repr)
+def test_residual_and_jacobi_sweeps(case):
+    h = case.handle()
+    try:
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        D = A.diagonal()
+        rng = np.random.default_rng(3)
+        b, x = rng.standard_normal(disc.ndof), rng.standard_normal(disc.ndof)
+        r = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        ig.igacd_residual(h, 0, to_dev(b), to_dev(x), r)
+        assert_close(to_host(r), b - A @ x, 1e-12, "residual")
+        omega = 0.37
+        xd = to_dev(x)
+        ig.igacd_smooth(h, 0, to_dev(b), xd, 3, omega)
+        xo = x.copy()
+        for _ in range(3):
+            xo = xo + omega * (b - A @ xo) / D
+        assert_close(to_host(xd), xo, 1e-12, "jacobi")
+    finally:
+        ig.igacd_destroy(h)
+
+
+VCYCLE_CASES = [Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels=2),   # config 0
+                Case(2, 3, 32, levels=3), Case(2, 4, 24, nu=1.0, beta=0.1, levels=2),
+                Case(3, 2, 8, nu=1.0, beta=0.1, levels=2), Case(3, 3, 8, nu=1.0, levels=2)]
+
+
+@pytest.mark.parametrize("case", VCYCLE_CASES, ids=repr)
+def test_vcycle_matches_oracle(case):
+    h = case.handle()
+    try:
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        H = Hierarchy(A, case.d, case.p, case.n, case.levels)
+        assert ig.igacd_num_levels(h) == len(H.ns)
+        for l in range(len(H.ns) - 1):
+            w, rho = ig.igacd_smoother_omega(h, l)
+            assert abs(rho - H.rho[l]) <= 1e-10 * H.rho[l], (l, rho, H.rho[l])
+        b = np.random.default_rng(11).uniform(-1, 1, disc.ndof)
+        x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        ig.igacd_vcycle(h, to_dev(b), x)
+        ref = H.vcycle(b)
+        assert_close(to_host(x), ref, 1e-12, "vcycle")
+    finally:
+        ig.igacd_destroy(h)
+
+
+SOLVE_CASES = [Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels=2),
+               Case(2, 3, 32, nu=1.0, beta=0.1, levels=0), Case(3, 2, 8, nu=1.0, beta=0.1, levels=2)]
+
+
+@pytest.mark.parametrize("case", SOLVE_CASES, ids=repr)
+def test_solve_matches_oracle(case):
+    h = case.handle()
+    try:
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        H = Hierarchy(A, case.d, case.p, case.n, case.levels)
+        b = np.random.default_rng(5).uniform(-1, 1, disc.ndof)
+        xo, ito, hist = pcg(A, b, H.vcycle, 1e-8, 2000)
+        x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        it, rel = ig.igacd_solve(h, to_dev(b), x, 1e-8, 2000)
+        xg = to_host(x)
+        assert abs(it - ito) <= 1, (it, ito)
+        assert rel < 1e-8
+        assert np.linalg.norm(b - A @ xg) / np.linalg.norm(b) < 1e-8 * 1.5
+        assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-8
+    finally:
+        ig.igacd_destroy(h)
+
+
+def test_solve_zero_rhs_and_host_api():
+    c = Case(2, 2, 8, levels=2)
+    h = c.handle()
+    try:
+        N = ig.igacd_ndof(h)
+        x = torch.ones(N, dtype=torch.float64, device="cuda")
+        it, rel = ig.igacd_solve(h, torch.zeros(N, dtype=torch.float64, device="cuda"), x, 1e-8, 10)
+        assert it == 0 and float(x.abs().max()) == 0.0
+        b = np.random.default_rng(0).standard_normal(N)
+        xh = np.zeros(N)
+        it1, rel1 = ig.igacd_solve_host(h, b, xh, 1e-10, 500)
+        xd = torch.zeros(N, dtype=torch.float64, device="cuda")
+        it2, rel2 = ig.igacd_solve(h, to_dev(b), xd, 1e-10, 500)
+        assert it1 == it2 and np.array_equal(xh, to_host(xd))
+    finally:
+        ig.igacd_destroy(h)
+
+
+def test_invalid_arguments_raise():
+    with pytest.raises(ig.IgacdError):
+        ig.igacd_create(2, 7, 8, 1, 0.1, 1, (1, 0))
+    with pytest.raises(ig.IgacdError):
+        ig.igacd_create(2, 2, 7, 1, 0.1, 1, (1, 0), levels=3)   # 7 is odd: cannot coarsen
+    h = Case(2, 2, 8, levels=2).handle()
+    try:
+        x = torch.zeros(ig.igacd_ndof(h), dtype=torch.float64, device="cuda")
+        with pytest.raises(ig.IgacdError):
+            ig.igacd_apply(h, 5, x, x.clone())
+        with pytest.raises(ig.IgacdError):
+            ig.igacd_apply(h, 0, x, x)
+    finally:
+        ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("ci", [1, 2, 3, 4])
+def test_full_size_config_apply_sampled(ci):
+    """BASELINE.json configs at full size, in the launch configuration bench.py times:
+    sampled output rows against the oracle's element integrals."""
+    c = inputs.config(ci)
+    h = ig.igacd_create(c.dim, c.p, c.n, c.nu, c.beta, c.lam, c.b0, levels=c.levels)
+    try:
+        N = ig.igacd_ndof(h)
+        assert N == c.ndof
+        x = to_dev(inputs.rhs(c))
+        y = torch.zeros(N, dtype=torch.float64, device="cuda")
+        ig.igacd_apply(h, 0, x, y)
+        disc = Discretization(c.dim, c.p, c.n)
+        dofs = sample_dofs(c.dim, c.m, 12 if c.dim == 3 else 24, seed=ci)
+        ref = disc.sampled_apply(form_alfven(c.nu, c.beta, c.lam, c.b0), inputs.rhs(c), dofs)
+        yg = to_host(y)
+        assert np.max(np.abs(yg[dofs] - ref)) <= 1e-12 * np.max(np.abs(ref))
+        # restriction / prolongation at full size: sampled entries of P^T x via the oracle's P_1D
+        # are covered at smaller sizes; here check linearity and symmetry of A at full size
+        z = to_dev(inputs.rhs(c, seed=99))
+        Az = torch.zeros_like(z)
+        ig.igacd_apply(h, 0, z, Az)
+        lhs, rhs = float(torch.dot(Az, x)), float(torch.dot(z, y))
+        assert abs(lhs - rhs) <= 1e-11 * (abs(lhs) + abs(rhs))
+    finally:
+        ig.igacd_destroy(h)
