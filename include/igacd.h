@@ -85,8 +85,24 @@ int igacd_restrict(igacd_handle h, int level, const double* x_fine, double* x_co
 /* x_fine = P_level x_coarse (accumulate == 0) or x_fine += P_level x_coarse (accumulate != 0). */
 int igacd_prolong(igacd_handle h, int level, const double* x_coarse, double* x_fine, int accumulate, void* stream);
 
-/* One V-cycle from a zero initial guess: x = B b, the preconditioner action (R6). */
+/* One V-cycle of the vector operator from a zero initial guess: x = V b (R6). */
 int igacd_vcycle(igacd_handle h, const double* b, double* x, void* stream);
+
+/* The PCG preconditioner action x = B b (reading R8).  Mode IGACD_PRECOND_VCYCLE: B = V.
+ * Mode IGACD_PRECOND_AUX (default when b0 != 0 and lambda > 0): symmetric multiplicative
+ * combination of the auxiliary-space correction on span{b0 s} -- the kernel of the lambda
+ * term -- with the V-cycle:  x = Pi Vs Pi^T b;  x += V(b - A x);  x += Pi Vs Pi^T (b - A x),
+ * Pi s = b0 s, Vs = V-cycle of the scalar operator A_s = Pi^T A Pi on the same levels. */
+#define IGACD_PRECOND_VCYCLE 0
+#define IGACD_PRECOND_AUX 1
+int igacd_precond(igacd_handle h, const double* b, double* x, void* stream);
+int igacd_set_preconditioner(igacd_handle h, int mode);
+int igacd_get_preconditioner(igacd_handle h, int* mode);
+
+/* Auxiliary scalar operator: s_out = A_s s_in on `level` (vectors of igacd_ndof/dim doubles),
+ * and its smoother parameters.  IGACD_E_ARG when the handle has no auxiliary space. */
+int igacd_apply_aux(igacd_handle h, int level, const double* s_in, double* s_out, void* stream);
+int igacd_aux_omega(igacd_handle h, int level, double* omega, double* rho);
 
 /* PCG with the V-cycle preconditioner, zero initial guess, stop when
  * ||r_k||_2 / ||r_0||_2 < tol or after maxit iterations (R7).

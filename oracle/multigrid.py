@@ -14,6 +14,13 @@ Readings (DESIGN.md):
   R5  coarsest level solved exactly (dense Cholesky, library primitive scipy cho_solve).
   R6  levels: n_{l+1} = n_l/2 while n_l is even, the next interior size n_l/2+p-2 >= 1 and
       d*(n_l+p-2)^d > 1500 (or exactly ``levels`` levels when requested).
+  R8  preconditioner: the V-cycle alone, or combined multiplicatively with a correction on the
+      auxiliary space span{b0 s} (the kernel of the lambda-term curl(b0 x u), which is exactly
+      representable: Pi s = b0 s maps the scalar spline space into V_h):
+          z = Pi Vs Pi^T r;  z += V (r - A z);  z += Pi Vs Pi^T (r - A z),
+      Vs = V-cycle of A_s := Pi^T A Pi on the same levels.  This is the paper's
+      multi-iterative idea ("basic iterative solvers having complementary
+      spectral behavior") applied to the near-kernel the L_A operator has.
 """
 import numpy as np
 import scipy.linalg as sla
@@ -50,13 +57,14 @@ def power_rho(A: sp.spmatrix, Ddiag: np.ndarray, steps: int = POWER_STEPS) -> fl
 
 
 class Hierarchy:
-    def __init__(self, A0: sp.spmatrix, d: int, p: int, n: int, levels: int = 0, nu_pre: int = 1, nu_post: int = 1):
+    def __init__(self, A0: sp.spmatrix, d: int, p: int, n: int, levels: int = 0, nu_pre: int = 1, nu_post: int = 1,
+                 ncomp: int = None, ns=None):
         self.d, self.p = d, p
-        self.ns = level_sizes(d, p, n, levels)
+        self.ns = level_sizes(d, p, n, levels) if ns is None else list(ns)
         self.A = [sp.csr_matrix(A0)]
         self.P = []
         for l in range(len(self.ns) - 1):
-            P = prolongation(d, p, self.ns[l + 1])
+            P = prolongation(d, p, self.ns[l + 1], ncomp)
             self.P.append(P)
             self.A.append(sp.csr_matrix(P.T @ self.A[l] @ P))      # A_{l+1} := P^T A_l P
         self.D = [A.diagonal().copy() for A in self.A]
@@ -86,3 +94,25 @@ class Hierarchy:
         x = x + self.P[l] @ e                                     #   prolongate and correct
         x = self.jacobi(l, b, x, self.nu_post)                    # step 3: post-smoothing
         return x
+
+
+def aux_map(d: int, nscal: int, b0) -> sp.csr_matrix:
+    """Pi: scalar coefficients s -> vector coefficients b0 s (component j = b0_j s)."""
+    return sp.vstack([b0[j] * sp.identity(nscal, format="csr") for j in range(d)]).tocsr()
+
+
+class AuxPreconditioner:
+    """Reading R8: z = Pi Vs Pi^T r;  z += V (r - A z);  z += Pi Vs Pi^T (r - A z)."""
+
+    def __init__(self, A0, d, p, n, b0, levels=0, nu_pre=1, nu_post=1):
+        self.A = sp.csr_matrix(A0)
+        self.V = Hierarchy(A0, d, p, n, levels, nu_pre, nu_post)
+        self.Pi = aux_map(d, A0.shape[0] // d, b0)
+        As = sp.csr_matrix(self.Pi.T @ self.A @ self.Pi)                # A_s := Pi^T A Pi
+        self.Vs = Hierarchy(As, d, p, n, levels, nu_pre, nu_post, ncomp=1, ns=self.V.ns)
+
+    def __call__(self, r):
+        z = self.Pi @ self.Vs.vcycle(self.Pi.T @ r)
+        z = z + self.V.vcycle(r - self.A @ z)
+        z = z + self.Pi @ self.Vs.vcycle(self.Pi.T @ (r - self.A @ z))
+        return z

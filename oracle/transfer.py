@@ -36,13 +36,14 @@ def prolongation_1d(p: int, n_coarse: int, full: bool = False) -> np.ndarray:
     return C[1:-1, 1:-1]
 
 
-def prolongation(d: int, p: int, n_coarse: int) -> sp.csr_matrix:
+def prolongation(d: int, p: int, n_coarse: int, ncomp: int = None) -> sp.csr_matrix:
     """I_d (x) P_1D (x) ... (x) P_1D  (eq:2by2prol); tiny entries
-    (|c| < 1e-14, rounding of exact zeros) are dropped."""
+    (|c| < 1e-14, rounding of exact zeros) are dropped.  ``ncomp`` components (default d;
+    1 for the scalar auxiliary space of reading R8)."""
     P1 = prolongation_1d(p, n_coarse)
     P1[np.abs(P1) < 1e-14] = 0.0
     P1s = sp.csr_matrix(P1)
     K = P1s
     for _ in range(d - 1):
         K = sp.kron(K, P1s, format="csr")
-    return sp.kron(sp.identity(d, format="csr"), K, format="csr")
+    return sp.kron(sp.identity(d if ncomp is None else ncomp, format="csr"), K, format="csr")

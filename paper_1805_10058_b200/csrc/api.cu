@@ -72,34 +72,36 @@ static std::vector<int> level_sizes(int d, int p, int n, int levels) {
   return ns;
 }
 
-static void destroy_handle(Handle* h) {
-  if (!h) return;
-  for (auto& L : h->lv) {
-    for (int f = 0; f < 3; ++f) cudaFree(L.band[f]);
+static void free_system(System& S) {
+  for (auto& L : S.lv) {
     cudaFree(L.b);
     cudaFree(L.x);
     cudaFree(L.t);
     cudaFree(L.r);
   }
+  cudaFree(S.cinv);
+  S.lv.clear();
+  S.cinv = nullptr;
+}
+
+static void destroy_handle(Handle* h) {
+  if (!h) return;
+  for (auto& L : h->lv)
+    for (int f = 0; f < 3; ++f) cudaFree(L.band[f]);
   for (auto& T : h->tr) {
     cudaFree(T.p_start);
     cudaFree(T.p_w);
     cudaFree(T.r_start);
     cudaFree(T.r_w);
   }
-  cudaFree(h->cinv);
+  free_system(h->sys[0]);
+  free_system(h->sys[1]);
   cudaFree(h->scratch0);
   cudaFree(h->scratch1);
   cudaFree(h->partial);
   cudaFree(h->scal);
   if (h->hscal) cudaFreeHost(h->hscal);
-  cudaFree(h->pr);
-  cudaFree(h->pz);
-  cudaFree(h->pp);
-  cudaFree(h->pq);
-  cudaFree(h->px);
-  cudaFree(h->pb);
-  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar}) cudaFree(v);
   for (auto& pr : h->ev_pending) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
@@ -116,29 +118,66 @@ static double reduce_to_host(Handle& h, int nparts, int slot, cudaStream_t s) {
   return h.hscal[slot];
 }
 
-static void estimate_omega(Handle& h, int l, cudaStream_t s) {
-  Level& L = h.lv[l];
+// Reading R4: rho_l = (v, A v)/(v, D v) after POWER_STEPS normalised steps v <- D^-1 A v / ||.||
+// from the counter-based start vector; omega_l = 4 / (3 * 1.05 * rho_l).
+static void estimate_omega(Handle& h, int sy, int l, cudaStream_t s) {
+  SysLevel& L = h.sys[sy].lv[l];
   double* v = L.x;
   double* w = L.t;
   launch_hash_vector(h, v, L.ndof, s);
   Epi ep{};
   ep.partial = h.partial;
   for (int it = 0; it < POWER_STEPS; ++it) {
-    const int np = launch_operator(h, l, v, w, EPI_DINV, DOT_OUT_OUT, ep, s);
+    const int np = launch_operator(h, sy, l, v, w, EPI_DINV, DOT_OUT_OUT, ep, s);
     launch_finalize(h, h.partial, np, h.scal + S_NORM, s);
     launch_scale(h, w, h.scal + S_NORM, nullptr, L.ndof, s);
     std::swap(v, w);
   }
-  const int np = launch_operator(h, l, v, w, EPI_APPLY, DOT_X_OUT, ep, s);
+  const int np = launch_operator(h, sy, l, v, w, EPI_APPLY, DOT_X_OUT, ep, s);
   const double vAv = reduce_to_host(h, np, S_A, s);
-  launch_dvdot(h, l, v, h.partial, s);
+  launch_dvdot(h, sy, l, v, h.partial, s);
   const double vDv = reduce_to_host(h, vec_ctas(L.ndof), S_B, s);
   L.rho = vAv / vDv;
   L.omega = 4.0 / (3.0 * 1.05 * L.rho);
 }
 
-static Handle* create_impl(int dim, int p, int n, const double* mass, const double* K, int levels, int nu_pre,
-                           int nu_post, cudaStream_t s) {
+static void setup_system(Handle& h, int sy, int nc, const Coef& coef, cudaStream_t s) {
+  System& S = h.sys[sy];
+  S.nc = nc;
+  S.coef = coef;
+  S.lv.resize(h.lv.size());
+  for (size_t l = 0; l < h.lv.size(); ++l) {
+    SysLevel& L = S.lv[l];
+    L.op = h.lv[l].geo;
+    L.op.c = coef;
+    L.ndof = (size_t)nc * h.lv[l].nscal;
+    IGACD_CUDA(cudaMalloc(&L.b, sizeof(double) * L.ndof));
+    IGACD_CUDA(cudaMalloc(&L.x, sizeof(double) * L.ndof));
+    IGACD_CUDA(cudaMalloc(&L.t, sizeof(double) * L.ndof));
+    IGACD_CUDA(cudaMalloc(&L.r, sizeof(double) * L.ndof));
+  }
+  // the dense coarse inverse is built only when the coarsest level is small enough;
+  // otherwise the system still applies its operator but refuses V-cycles
+  if (S.lv.back().ndof <= COARSE_DENSE_MAX) build_coarse_inverse(h, sy, s);
+  for (size_t l = 0; l + 1 < h.lv.size(); ++l) estimate_omega(h, sy, (int)l, s);
+}
+
+// Reading R8: patterns of A_s = Pi^T A Pi, Pi s = b0 s:  C_s = sum_ij b0_i C[i][j] b0_j.
+static Coef aux_patterns(int d, const Coef& c, const double* b0) {
+  Coef a;
+  std::memset(&a, 0, sizeof(a));
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) {
+      const double w = b0[i] * b0[j];
+      a.mass[0][0] += w * c.mass[i][j];
+      for (int l = 0; l < 3; ++l) a.S[l][0][0] += w * c.S[l][i][j];
+      for (int q = 0; q < 3; ++q) a.AA[q][0][0] += w * c.AA[q][i][j];
+    }
+  return a;
+}
+
+static Handle* create_impl(int dim, int p, int n, const double* mass, const double* K, const double* b0, int levels,
+                           int nu_pre, int nu_post, cudaStream_t s) {
   if (dim != 2 && dim != 3) throw Error{IGACD_E_ARG, "dim must be 2 or 3"};
   if (p < 1 || p > MAXP) throw Error{IGACD_E_ARG, "p must be in [1, 6]"};
   if (n < 1 || n + p - 2 < 1) throw Error{IGACD_E_ARG, "need n >= 1 and n + p - 2 >= 1"};
@@ -150,23 +189,22 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
     h->nu_pre = nu_pre;
     h->nu_post = nu_post;
     h->stream = s;
-    h->coef = patterns(dim, mass, K);
+    double bb = 0.0;
+    if (b0)
+      for (int j = 0; j < dim; ++j) {
+        h->b0[j] = b0[j];
+        bb += b0[j] * b0[j];
+      }
+    const Coef coef = patterns(dim, mass, K);
     const std::vector<int> ns = level_sizes(dim, p, n, levels);
     h->lv.resize(ns.size());
-    size_t maxndof = 0;
     for (size_t l = 0; l < ns.size(); ++l) {
       Level& L = h->lv[l];
       L.n = ns[l];
       L.m = ns[l] + p - 2;
       L.nscal = 1;
       for (int a = 0; a < dim; ++a) L.nscal *= (size_t)L.m;
-      L.ndof = dim * L.nscal;
-      maxndof = std::max(maxndof, L.ndof);
       assemble_level(*h, L, s);
-      IGACD_CUDA(cudaMalloc(&L.b, sizeof(double) * L.ndof));
-      IGACD_CUDA(cudaMalloc(&L.x, sizeof(double) * L.ndof));
-      IGACD_CUDA(cudaMalloc(&L.t, sizeof(double) * L.ndof));
-      IGACD_CUDA(cudaMalloc(&L.r, sizeof(double) * L.ndof));
     }
     h->tr.resize(ns.size() - 1);
     size_t scratch = 1;
@@ -181,21 +219,20 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
     size_t np = 1;
     for (size_t l = 0; l < ns.size(); ++l) {
       np = std::max(np, (size_t)operator_ctas(*h, (int)l));
-      np = std::max(np, (size_t)vec_ctas(h->lv[l].ndof));
+      np = std::max(np, (size_t)vec_ctas((size_t)dim * h->lv[l].nscal));
     }
     h->partial_len = np;
     IGACD_CUDA(cudaMalloc(&h->partial, sizeof(double) * np));
     IGACD_CUDA(cudaMalloc(&h->scal, sizeof(double) * NSLOT));
     IGACD_CUDA(cudaMallocHost(&h->hscal, sizeof(double) * NSLOT));
-    const size_t n0 = h->lv[0].ndof;
-    IGACD_CUDA(cudaMalloc(&h->pr, sizeof(double) * n0));
-    IGACD_CUDA(cudaMalloc(&h->pz, sizeof(double) * n0));
-    IGACD_CUDA(cudaMalloc(&h->pp, sizeof(double) * n0));
-    IGACD_CUDA(cudaMalloc(&h->pq, sizeof(double) * n0));
-    // the dense coarse inverse is built only when the coarsest level is small enough;
-    // otherwise the handle still applies the operator but refuses V-cycles / solves
-    if (h->lv.back().ndof <= COARSE_DENSE_MAX) build_coarse_inverse(*h, s);
-    for (size_t l = 0; l + 1 < ns.size(); ++l) estimate_omega(*h, (int)l, s);
+    const size_t n0 = (size_t)dim * h->lv[0].nscal;
+    for (double** v : {&h->pr, &h->pz, &h->pp, &h->pq, &h->aw, &h->ar}) IGACD_CUDA(cudaMalloc(v, sizeof(double) * n0));
+    setup_system(*h, 0, dim, coef, s);
+    // auxiliary space span{b0 s} (reading R8) when the b0-term is present
+    const Coef ac = aux_patterns(dim, coef, h->b0);
+    h->has_aux = bb > 0.0 && ac.mass[0][0] + ac.S[0][0][0] + ac.S[1][0][0] + ac.S[2][0][0] > 0.0;
+    if (h->has_aux) setup_system(*h, 1, 1, ac, s);
+    h->precond = h->has_aux ? PRECOND_AUX : PRECOND_VCYCLE;
     IGACD_CUDA(cudaStreamSynchronize(s));
   } catch (...) {
     destroy_handle(h);
@@ -205,53 +242,79 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
 }
 
 // ---- V-cycle ------------------------------------------------------------------------------
-static void jacobi_sweeps(Handle& h, int l, const double* b, double*& cur, double*& oth, int sweeps, double omega,
-                          cudaStream_t s) {
+static void jacobi_sweeps(Handle& h, int sy, int l, const double* b, double*& cur, double*& oth, int sweeps,
+                          double omega, cudaStream_t s) {
   Epi ep{};
   ep.omega = omega;
   ep.b = b;
   for (int k = 0; k < sweeps; ++k) {
-    launch_operator(h, l, cur, oth, EPI_JACOBI, DOT_NONE, ep, s);
+    launch_operator(h, sy, l, cur, oth, EPI_JACOBI, DOT_NONE, ep, s);
     std::swap(cur, oth);
   }
 }
 
 // x = V_l b from a zero initial guess (pre-smooth, residual,
 // restrict, recurse, prolongate-and-correct, post-smooth).  The result lands in x.
-static void vcycle_level(Handle& h, int l, const double* b, double* x, cudaStream_t s) {
-  const int Lc = (int)h.lv.size() - 1;
-  if (!h.cinv)
+static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, cudaStream_t s) {
+  System& S = h.sys[sy];
+  const int Lc = (int)S.lv.size() - 1;
+  if (!S.cinv)
     throw Error{IGACD_E_ARG, "coarsest level too large for the dense coarse solver (" +
-                                 std::to_string(h.lv.back().ndof) + " dofs); choose n divisible by a higher power of 2"};
+                                 std::to_string(S.lv.back().ndof) + " dofs); choose n divisible by a higher power of 2"};
   if (l == Lc) {
-    launch_coarse_solve(h, b, x, s);
+    launch_coarse_solve(h, sy, b, x, s);
     return;
   }
-  Level& L = h.lv[l];
+  SysLevel& L = S.lv[l];
   const int swaps = std::max(0, h.nu_pre - 1) + h.nu_post;
   double* cur = (swaps % 2 == 0) ? x : L.t;
   double* oth = (cur == x) ? L.t : x;
   if (h.nu_pre >= 1) {
-    launch_scale_dinv(h, l, b, cur, L.omega, s);   // first sweep from x = 0: x = omega D^-1 b
-    jacobi_sweeps(h, l, b, cur, oth, h.nu_pre - 1, L.omega, s);
+    launch_scale_dinv(h, sy, l, b, cur, L.omega, s);   // first sweep from x = 0: x = omega D^-1 b
+    jacobi_sweeps(h, sy, l, b, cur, oth, h.nu_pre - 1, L.omega, s);
   } else {
     launch_zero(h, cur, L.ndof, s);
   }
   Epi ep{};
   ep.b = b;
-  launch_operator(h, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
-  Level& C = h.lv[l + 1];
-  launch_restrict(h, l, L.r, C.b, s);
-  vcycle_level(h, l + 1, C.b, C.x, s);
-  launch_prolong(h, l, C.x, cur, true, s);
-  jacobi_sweeps(h, l, b, cur, oth, h.nu_post, L.omega, s);
+  launch_operator(h, sy, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
+  SysLevel& C = S.lv[l + 1];
+  launch_restrict(h, S.nc, l, L.r, C.b, s);
+  vcycle_level(h, sy, l + 1, C.b, C.x, s);
+  launch_prolong(h, S.nc, l, C.x, cur, true, s);
+  jacobi_sweeps(h, sy, l, b, cur, oth, h.nu_post, L.omega, s);
   if (cur != x) launch_copy(h, cur, x, L.ndof, s);
+}
+
+// Preconditioner action z = B r (reading R8).  PRECOND_VCYCLE: B = V.  PRECOND_AUX: the
+// symmetric multiplicative combination of the auxiliary-space correction on span{b0 s}
+// (B_s = scalar V-cycle of A_s = Pi^T A Pi) and the vector V-cycle:
+//   z = Pi B_s Pi^T r;  z += V (r - A z);  z += Pi B_s Pi^T (r - A z).
+static void precond_apply(Handle& h, const double* r, double* z, cudaStream_t s) {
+  if (h.precond == PRECOND_VCYCLE || !h.has_aux) {
+    vcycle_level(h, 0, 0, r, z, s);
+    return;
+  }
+  System& A = h.sys[1];
+  SysLevel& a0 = A.lv[0];
+  Epi ep{};
+  ep.b = r;
+  launch_pi_t(h, r, a0.b, s);
+  vcycle_level(h, 1, 0, a0.b, a0.x, s);
+  launch_pi(h, a0.x, z, false, s);
+  launch_operator(h, 0, 0, z, h.ar, EPI_RESID, DOT_NONE, ep, s);
+  vcycle_level(h, 0, 0, h.ar, h.aw, s);
+  launch_axpy_inplace(h, h.aw, z, h.lv.empty() ? 0 : h.sys[0].lv[0].ndof, s);
+  launch_operator(h, 0, 0, z, h.ar, EPI_RESID, DOT_NONE, ep, s);
+  launch_pi_t(h, h.ar, a0.b, s);
+  vcycle_level(h, 1, 0, a0.b, a0.x, s);
+  launch_pi(h, a0.x, z, true, s);
 }
 
 // ---- PCG ---------------------------------------------------------------------------------
 static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
                cudaStream_t s) {
-  const size_t N = h.lv[0].ndof;
+  const size_t N = h.sys[0].lv[0].ndof;
   const int nv = vec_ctas(N);
   launch_copy(h, b, h.pr, N, s);
   launch_dot(h, h.pr, h.pr, N, h.partial, s);
@@ -261,7 +324,7 @@ static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int
   if (iters) *iters = 0;
   if (relres) *relres = 0.0;
   if (r0 == 0.0) return IGACD_OK;
-  vcycle_level(h, 0, h.pr, h.pz, s);
+  precond_apply(h, h.pr, h.pz, s);
   launch_dot(h, h.pr, h.pz, N, h.partial, s);
   int rz = S_RZ0;
   launch_finalize(h, h.partial, nv, h.scal + rz, s);
@@ -277,7 +340,7 @@ static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int
       IGACD_CUDA(cudaEventCreate(&e1));
       IGACD_CUDA(cudaEventRecord(e0, s));
     }
-    const int np = launch_operator(h, 0, h.pp, h.pq, EPI_APPLY, DOT_X_OUT, ep, s);
+    const int np = launch_operator(h, 0, 0, h.pp, h.pq, EPI_APPLY, DOT_X_OUT, ep, s);
     h.apply_launches++;
     if (h.profiling) {
       IGACD_CUDA(cudaEventRecord(e1, s));
@@ -289,7 +352,7 @@ static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int
     rel = std::sqrt(rr) / r0;
     if (rel < tol) break;
     if (it == maxit) break;
-    vcycle_level(h, 0, h.pr, h.pz, s);
+    precond_apply(h, h.pr, h.pz, s);
     launch_dot(h, h.pr, h.pz, N, h.partial, s);
     const int rzn = rz == S_RZ0 ? S_RZ1 : S_RZ0;
     launch_finalize(h, h.partial, nv, h.scal + rzn, s);
@@ -353,7 +416,8 @@ int igacd_create(igacd_handle* out, int dim, int p, int n, double nu, double bet
   if (!(nu >= 0 && beta >= 0 && lambda >= 0)) throw Error{IGACD_E_ARG, "nu, beta, lambda must be >= 0"};
   double mass[9], K[81];
   alfven_form(dim, nu, beta, lambda, b0, mass, K);
-  *out = reinterpret_cast<igacd_handle>(create_impl(dim, p, n, mass, K, levels, nu_pre, nu_post, (cudaStream_t)stream));
+  *out = reinterpret_cast<igacd_handle>(
+      create_impl(dim, p, n, mass, K, b0, levels, nu_pre, nu_post, (cudaStream_t)stream));
   API_END
 }
 
@@ -364,7 +428,8 @@ int igacd_create_form(igacd_handle* out, int dim, int p, int n, const double* ma
   *out = nullptr;
   check_ptr(mass);
   check_ptr(K);
-  *out = reinterpret_cast<igacd_handle>(create_impl(dim, p, n, mass, K, levels, nu_pre, nu_post, (cudaStream_t)stream));
+  *out = reinterpret_cast<igacd_handle>(
+      create_impl(dim, p, n, mass, K, nullptr, levels, nu_pre, nu_post, (cudaStream_t)stream));
   API_END
 }
 
@@ -405,15 +470,15 @@ int igacd_ndof(igacd_handle h, int level, size_t* ndof) {
   API_BEGIN
   check_ptr(ndof);
   check_level(H(h), level);
-  *ndof = H(h)->lv[level].ndof;
+  *ndof = H(h)->sys[0].lv[level].ndof;
   API_END
 }
 
 int igacd_smoother_omega(igacd_handle h, int level, double* omega, double* rho) {
   API_BEGIN
   check_level(H(h), level);
-  if (omega) *omega = H(h)->lv[level].omega;
-  if (rho) *rho = H(h)->lv[level].rho;
+  if (omega) *omega = H(h)->sys[0].lv[level].omega;
+  if (rho) *rho = H(h)->sys[0].lv[level].rho;
   API_END
 }
 
@@ -425,7 +490,7 @@ int igacd_apply(igacd_handle h, int level, const double* x, double* y, void* str
   check_ptr(y);
   if (x == y) throw Error{IGACD_E_ARG, "x and y must not alias"};
   Epi ep{};
-  launch_operator(*hh, level, x, y, EPI_APPLY, DOT_NONE, ep, (cudaStream_t)stream);
+  launch_operator(*hh, 0, level, x, y, EPI_APPLY, DOT_NONE, ep, (cudaStream_t)stream);
   API_END
 }
 
@@ -439,7 +504,7 @@ int igacd_residual(igacd_handle h, int level, const double* b, const double* x, 
   if (r == x || r == b) throw Error{IGACD_E_ARG, "r must not alias b or x"};
   Epi ep{};
   ep.b = b;
-  launch_operator(*hh, level, x, r, EPI_RESID, DOT_NONE, ep, (cudaStream_t)stream);
+  launch_operator(*hh, 0, level, x, r, EPI_RESID, DOT_NONE, ep, (cudaStream_t)stream);
   API_END
 }
 
@@ -450,12 +515,12 @@ int igacd_smooth(igacd_handle h, int level, const double* b, double* x, int swee
   check_ptr(b);
   check_ptr(x);
   if (sweeps < 0) throw Error{IGACD_E_ARG, "negative sweeps"};
-  Level& L = hh->lv[level];
+  SysLevel& L = hh->sys[0].lv[level];
   const double w = omega > 0 ? omega : L.omega;
   if (!(w > 0)) throw Error{IGACD_E_ARG, "no smoother parameter on this level; pass omega > 0"};
   double* cur = x;
   double* oth = L.t;
-  jacobi_sweeps(*hh, level, b, cur, oth, sweeps, w, (cudaStream_t)stream);
+  jacobi_sweeps(*hh, 0, level, b, cur, oth, sweeps, w, (cudaStream_t)stream);
   if (cur != x) launch_copy(*hh, cur, x, L.ndof, (cudaStream_t)stream);
   API_END
 }
@@ -466,7 +531,7 @@ int igacd_restrict(igacd_handle h, int level, const double* x_fine, double* x_co
   check_level(hh, level, true);
   check_ptr(x_fine);
   check_ptr(x_coarse);
-  launch_restrict(*hh, level, x_fine, x_coarse, (cudaStream_t)stream);
+  launch_restrict(*hh, hh->dim, level, x_fine, x_coarse, (cudaStream_t)stream);
   API_END
 }
 
@@ -476,7 +541,7 @@ int igacd_prolong(igacd_handle h, int level, const double* x_coarse, double* x_f
   check_level(hh, level, true);
   check_ptr(x_fine);
   check_ptr(x_coarse);
-  launch_prolong(*hh, level, x_coarse, x_fine, accumulate != 0, (cudaStream_t)stream);
+  launch_prolong(*hh, hh->dim, level, x_coarse, x_fine, accumulate != 0, (cudaStream_t)stream);
   API_END
 }
 
@@ -486,7 +551,55 @@ int igacd_vcycle(igacd_handle h, const double* b, double* x, void* stream) {
   check_ptr(b);
   check_ptr(x);
   if (b == x) throw Error{IGACD_E_ARG, "b and x must not alias"};
-  vcycle_level(*hh, 0, b, x, (cudaStream_t)stream);
+  vcycle_level(*hh, 0, 0, b, x, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_precond(igacd_handle h, const double* b, double* x, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_ptr(b);
+  check_ptr(x);
+  if (b == x) throw Error{IGACD_E_ARG, "b and x must not alias"};
+  precond_apply(*hh, b, x, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_set_preconditioner(igacd_handle h, int mode) {
+  API_BEGIN
+  Handle* hh = H(h);
+  if (mode != PRECOND_VCYCLE && mode != PRECOND_AUX) throw Error{IGACD_E_ARG, "unknown preconditioner"};
+  if (mode == PRECOND_AUX && !hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space (b0 = 0 or lambda = 0)"};
+  hh->precond = mode;
+  API_END
+}
+
+int igacd_get_preconditioner(igacd_handle h, int* mode) {
+  API_BEGIN
+  check_ptr(mode);
+  *mode = H(h)->precond;
+  API_END
+}
+
+int igacd_apply_aux(igacd_handle h, int level, const double* s_in, double* s_out, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level);
+  check_ptr(s_in);
+  check_ptr(s_out);
+  if (!hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space on this handle"};
+  Epi ep{};
+  launch_operator(*hh, 1, level, s_in, s_out, EPI_APPLY, DOT_NONE, ep, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_aux_omega(igacd_handle h, int level, double* omega, double* rho) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level);
+  if (!hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space on this handle"};
+  if (omega) *omega = hh->sys[1].lv[level].omega;
+  if (rho) *rho = hh->sys[1].lv[level].rho;
   API_END
 }
 
@@ -514,7 +627,7 @@ int igacd_solve_host(igacd_handle h, const double* b_host, double* x_host, doubl
   check_ptr(x_host);
   if (!(tol > 0) || maxit < 1) throw Error{IGACD_E_ARG, "need tol > 0 and maxit >= 1"};
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t N = hh->lv[0].ndof;
+  const size_t N = hh->sys[0].lv[0].ndof;
   if (!hh->px) IGACD_CUDA(cudaMalloc(&hh->px, sizeof(double) * N));
   if (!hh->pb) IGACD_CUDA(cudaMalloc(&hh->pb, sizeof(double) * N));
   IGACD_CUDA(cudaMemcpyAsync(hh->pb, b_host, sizeof(double) * N, cudaMemcpyHostToDevice, s));

@@ -20,14 +20,14 @@ namespace igacd {
 // ---------------------------------------------------------------------------------------
 // 2D
 // ---------------------------------------------------------------------------------------
-template <int P, int NT>
+template <int P, int NT, int NC>
 __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, int mode, int dot,
                                              const double* __restrict__ x, double* __restrict__ y,
                                              int chunk) {
   constexpr int R = 2 * P + 1;
   constexpr int W = NT + 2 * P;
   constexpr int LPT = (W + NT - 1) / NT;
-  __shared__ double xs[2][2][W];
+  __shared__ double xs[2][NC][W];
   __shared__ double red[NT / 32];
   const int m = op.m;
   const size_t ms = (size_t)m * m;
@@ -41,15 +41,17 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
   const int se = c1 + P;
   const bool zone = active && (k < op.zoneL || k >= op.zoneR);
 
-  double acc0[R], acc1[R];
+  double acc[NC][R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc0[r] = acc1[r] = 0.0;
+  for (int i = 0; i < NC; ++i)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[i][r] = 0.0;
   double dsum = 0.0;
-  double pre[2][LPT];
+  double pre[NC][LPT];
 
   auto gload = [&](int s) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NC; ++j)
 #pragma unroll
       for (int i = 0; i < LPT; ++i) {
         const int idx = tid + i * NT;
@@ -61,7 +63,7 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
   };
   auto sstore = [&](int buf) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NC; ++j)
 #pragma unroll
       for (int i = 0; i < LPT; ++i) {
         const int idx = tid + i * NT;
@@ -81,11 +83,11 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
         const bool more = s + 1 < se;
         if (more) gload(s + 1);
         if (s < m) {
-          double zM[2], zS[2], zA[2];
+          double zM[NC], zS[NC], zA[NC];
           {
-            double uM[2], uS[2], uA[2];
+            double uM[NC], uS[NC], uA[NC];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < NC; ++j) {
               const double* xr = &xs[buf][j][tid + P];
               const double xc = xr[0];
               double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
@@ -115,11 +117,14 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
               uA[j] = va;
             }
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              zM[i] = op.c.mass[i][0] * uM[0] + op.c.mass[i][1] * uM[1] + op.c.S[1][i][0] * uS[0] +
-                      op.c.S[1][i][1] * uS[1];
-              zS[i] = op.c.S[0][i][0] * uM[0] + op.c.S[0][i][1] * uM[1];
-              zA[i] = op.c.AA[0][i][0] * uA[0] + op.c.AA[0][i][1] * uA[1];
+            for (int i = 0; i < NC; ++i) {
+              zM[i] = zS[i] = zA[i] = 0.0;
+#pragma unroll
+              for (int j = 0; j < NC; ++j) {
+                zM[i] = fma(op.c.mass[i][j], uM[j], fma(op.c.S[1][i][j], uS[j], zM[i]));
+                zS[i] = fma(op.c.S[0][i][j], uM[j], zS[i]);
+                zA[i] = fma(op.c.AA[0][i][j], uA[j], zA[i]);
+              }
             }
           }
 #pragma unroll
@@ -129,8 +134,8 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
               const size_t wi = (size_t)t * R + P - o;   // F[t][s], s - t = -o
               const double wM = __ldg(op.bM + wi), wS = __ldg(op.bS + wi), wA = __ldg(op.bA + wi);
               const int slot = (ph + o + R) % R;
-              acc0[slot] = fma(wM, zM[0], fma(wS, zS[0], fma(wA, zA[0], acc0[slot])));
-              acc1[slot] = fma(wM, zM[1], fma(wS, zS[1], fma(wA, zA[1], acc1[slot])));
+#pragma unroll
+              for (int i = 0; i < NC; ++i) acc[i][slot] = fma(wM, zM[i], fma(wS, zS[i], fma(wA, zA[i], acc[i][slot])));
             }
           }
         }
@@ -139,17 +144,20 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
           const int slot = (ph + R - P) % R;
           if (t >= c0 && t < c1 && active) {
             const size_t pt = (size_t)t * m + k;
-            double D0 = 1.0, D1 = 1.0;
+            double Dv[NC];
+#pragma unroll
+            for (int i = 0; i < NC; ++i) Dv[i] = 1.0;
             if (mode >= EPI_JACOBI) {
               const double Mt = __ldg(op.bM + (size_t)t * R + P), St = __ldg(op.bS + (size_t)t * R + P);
               const double Mk = __ldg(op.bM + (size_t)k * R + P), Sk = __ldg(op.bS + (size_t)k * R + P);
-              D0 = op.c.mass[0][0] * Mt * Mk + op.c.S[0][0][0] * St * Mk + op.c.S[1][0][0] * Mt * Sk;
-              D1 = op.c.mass[1][1] * Mt * Mk + op.c.S[0][1][1] * St * Mk + op.c.S[1][1][1] * Mt * Sk;
+#pragma unroll
+              for (int i = 0; i < NC; ++i)
+                Dv[i] = op.c.mass[i][i] * Mt * Mk + op.c.S[0][i][i] * St * Mk + op.c.S[1][i][i] * Mt * Sk;
             }
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const double a = i == 0 ? acc0[slot] : acc1[slot];
-              const double D = i == 0 ? D0 : D1;
+            for (int i = 0; i < NC; ++i) {
+              const double a = acc[i][slot];
+              const double D = Dv[i];
               const size_t gi = (size_t)i * ms + pt;
               double out;
               if (mode == EPI_APPLY) out = a;
@@ -161,8 +169,8 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
               else if (dot == DOT_OUT_OUT) dsum = fma(out, out, dsum);
             }
           }
-          acc0[slot] = 0.0;
-          acc1[slot] = 0.0;
+#pragma unroll
+          for (int i = 0; i < NC; ++i) acc[i][slot] = 0.0;
         }
         if (more) sstore(buf ^ 1);
         __syncthreads();
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
 // ---------------------------------------------------------------------------------------
 // 3D
 // ---------------------------------------------------------------------------------------
-template <int P, int T2, int T3>
+template <int P, int T2, int T3, int NC>
 struct Op3dShape {
   static constexpr int NT = T2 * T3;
   static constexpr int R = 2 * P + 1;
@@ -193,20 +201,20 @@ struct Op3dShape {
   static constexpr int HC = T3 + 2 * P;
   static constexpr int XS = HR * HC;        // one component of one slab tile
   static constexpr int US = T2 * HC;        // one stage-A output array
-  static constexpr int SMEM = (2 * 3 * XS + 9 * US) * 8 + (NT / 32) * 8;
-  static constexpr int LPT = (3 * XS + NT - 1) / NT;
+  static constexpr int SMEM = (2 * NC * XS + 3 * NC * US) * 8 + (NT / 32) * 8;
+  static constexpr int LPT = (NC * XS + NT - 1) / NT;
 };
 
-template <int P, int T2, int T3>
+template <int P, int T2, int T3, int NC>
 __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep, int mode, int dot,
                                                  const double* __restrict__ x, double* __restrict__ y,
                                                  int chunk) {
-  using Sh = Op3dShape<P, T2, T3>;
-  constexpr int NT = Sh::NT, R = Sh::R, HR = Sh::HR, HC = Sh::HC, XS = Sh::XS, US = Sh::US, LPT = Sh::LPT;
+  using Sh = Op3dShape<P, T2, T3, NC>;
+  constexpr int NT = Sh::NT, R = Sh::R, HC = Sh::HC, XS = Sh::XS, US = Sh::US, LPT = Sh::LPT;
   extern __shared__ double smem[];
-  double* xs = smem;                  // [2][3][HR][HC]
-  double* us = smem + 2 * 3 * XS;     // [9][T2][HC]: index (F*3 + j), F: 0 M, 1 S, 2 A
-  double* red = us + 9 * US;
+  double* xs = smem;                   // [2][NC][HR][HC]
+  double* us = smem + 2 * NC * XS;     // [3][NC][T2][HC]: index (F*NC + j), F: 0 M, 1 S, 2 A
+  double* red = us + 3 * NC * US;
   const int m = op.m;
   const size_t ms = (size_t)m * m;
   const size_t m3 = ms * m;
@@ -221,9 +229,9 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
   const int sb = max(0, c0 - P);
   const int se = c1 + P;
 
-  double acc[3][R];
+  double acc[NC][R];
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < NC; ++i)
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[i][r] = 0.0;
   double dsum = 0.0;
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
     for (int i = 0; i < LPT; ++i) {
       const int idx = tid + i * NT;
       double v = 0.0;
-      if (idx < 3 * XS && s < m) {
+      if (idx < NC * XS && s < m) {
         const int j = idx / XS, rem = idx % XS;
         const int hr = rem / HC, hc = rem % HC;
         const int g1 = r0 - P + hr, g2 = q0 - P + hc;
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
 #pragma unroll
     for (int i = 0; i < LPT; ++i) {
       const int idx = tid + i * NT;
-      if (idx < 3 * XS) xs[buf * 3 * XS + idx] = pre[i];
+      if (idx < NC * XS) xs[buf * NC * XS + idx] = pre[i];
     }
   };
 
@@ -269,8 +277,8 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
             const int g1 = r0 + r;
             const bool zoneA = g1 < m && (g1 < op.zoneL || g1 >= op.zoneR);
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              const double* xc_ = xs + buf * 3 * XS + j * XS + (r + P) * HC + cc;
+            for (int j = 0; j < NC; ++j) {
+              const double* xc_ = xs + buf * NC * XS + j * XS + (r + P) * HC + cc;
               const double xc = xc_[0];
               double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
 #pragma unroll
@@ -294,19 +302,21 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
                   va = fma(__ldg(rA + o), v, va);
                 }
               }
-              us[(0 * 3 + j) * US + it] = vm;
-              us[(1 * 3 + j) * US + it] = vs;
-              us[(2 * 3 + j) * US + it] = va;
+              us[(0 * NC + j) * US + it] = vm;
+              us[(1 * NC + j) * US + it] = vs;
+              us[(2 * NC + j) * US + it] = va;
             }
           }
           __syncthreads();
           // ---- stage B: contract direction 2, combine patterns into z_{i,F0}
-          double zM[3] = {0, 0, 0}, zS[3] = {0, 0, 0}, zA[3] = {0, 0, 0};
+          double zM[NC], zS[NC], zA[NC];
 #pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            const double* uM = us + (0 * 3 + j) * US + tr * HC + tc + P;
-            const double* uS = us + (1 * 3 + j) * US + tr * HC + tc + P;
-            const double* uA = us + (2 * 3 + j) * US + tr * HC + tc + P;
+          for (int i = 0; i < NC; ++i) zM[i] = zS[i] = zA[i] = 0.0;
+#pragma unroll
+          for (int j = 0; j < NC; ++j) {
+            const double* uM = us + (0 * NC + j) * US + tr * HC + tc + P;
+            const double* uS = us + (1 * NC + j) * US + tr * HC + tc + P;
+            const double* uA = us + (2 * NC + j) * US + tr * HC + tc + P;
             double vMM, vMS, vMA, vSM, vAM, vAA;
             {
               const double c = uM[0];
@@ -355,7 +365,7 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
               }
             }
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {
+            for (int i = 0; i < NC; ++i) {
               zM[i] = fma(op.c.mass[i][j], vMM, zM[i]);
               zS[i] = fma(op.c.S[0][i][j], vMM, zS[i]);
               zM[i] = fma(op.c.S[1][i][j], vSM, zM[i]);
@@ -374,7 +384,7 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
               const double wM = __ldg(op.bM + wi), wS = __ldg(op.bS + wi), wA = __ldg(op.bA + wi);
               const int slot = (ph + o + R) % R;
 #pragma unroll
-              for (int i = 0; i < 3; ++i) acc[i][slot] = fma(wM, zM[i], fma(wS, zS[i], fma(wA, zA[i], acc[i][slot])));
+              for (int i = 0; i < NC; ++i) acc[i][slot] = fma(wM, zM[i], fma(wS, zS[i], fma(wA, zA[i], acc[i][slot])));
             }
           }
         }
@@ -383,18 +393,20 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
           const int slot = (ph + R - P) % R;
           if (t >= c0 && t < c1 && active) {
             const size_t pt = (size_t)t * ms + (size_t)gr * m + gc;
-            double Dv[3] = {1.0, 1.0, 1.0};
+            double Dv[NC];
+#pragma unroll
+            for (int i = 0; i < NC; ++i) Dv[i] = 1.0;
             if (mode >= EPI_JACOBI) {
               const double M0 = __ldg(op.bM + (size_t)t * R + P), S0 = __ldg(op.bS + (size_t)t * R + P);
               const double M1 = __ldg(op.bM + (size_t)gr * R + P), S1 = __ldg(op.bS + (size_t)gr * R + P);
               const double M2 = __ldg(op.bM + (size_t)gc * R + P), S2 = __ldg(op.bS + (size_t)gc * R + P);
 #pragma unroll
-              for (int i = 0; i < 3; ++i)
+              for (int i = 0; i < NC; ++i)
                 Dv[i] = op.c.mass[i][i] * M0 * M1 * M2 + op.c.S[0][i][i] * S0 * M1 * M2 +
                         op.c.S[1][i][i] * M0 * S1 * M2 + op.c.S[2][i][i] * M0 * M1 * S2;
             }
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {
+            for (int i = 0; i < NC; ++i) {
               const double a = acc[i][slot];
               const size_t gi = (size_t)i * m3 + pt;
               double out;
@@ -408,7 +420,7 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
             }
           }
 #pragma unroll
-          for (int i = 0; i < 3; ++i) acc[i][slot] = 0.0;
+          for (int i = 0; i < NC; ++i) acc[i][slot] = 0.0;
         }
         if (more) sstore(buf ^ 1);
         __syncthreads();
@@ -466,50 +478,52 @@ int operator_ctas(const Handle& h, int level) {
   return g.grid.x * g.grid.y * g.grid.z;
 }
 
-template <int P>
+template <int P, int NC>
 static void launch2d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
                      cudaStream_t s) {
-  k_op2d<P, NT2D><<<g.grid, NT2D, 0, s>>>(op, ep, mode, dot, x, y, g.chunk);
+  k_op2d<P, NT2D, NC><<<g.grid, NT2D, 0, s>>>(op, ep, mode, dot, x, y, g.chunk);
+}
+
+template <int P, int NC>
+static void launch3d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                     cudaStream_t s) {
+  using Sh = Op3dShape<P, T2_3D, T3_3D, NC>;
+  static bool attr = false;
+  if (!attr) {
+    IGACD_CUDA(cudaFuncSetAttribute(k_op3d<P, T2_3D, T3_3D, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Sh::SMEM));
+    attr = true;
+  }
+  k_op3d<P, T2_3D, T3_3D, NC><<<g.grid, Sh::NT, Sh::SMEM, s>>>(op, ep, mode, dot, x, y, g.chunk);
 }
 
 template <int P>
-static void launch3d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
-                     cudaStream_t s) {
-  using Sh = Op3dShape<P, T2_3D, T3_3D>;
-  static bool attr = false;
-  if (!attr) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_op3d<P, T2_3D, T3_3D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM));
-    attr = true;
+static void dispatch(int dim, int nc, const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot,
+                     const double* x, double* y, cudaStream_t s) {
+  if (dim == 2) {
+    if (nc == 1) launch2d<P, 1>(g, op, ep, mode, dot, x, y, s);
+    else launch2d<P, 2>(g, op, ep, mode, dot, x, y, s);
+  } else {
+    if (nc == 1) launch3d<P, 1>(g, op, ep, mode, dot, x, y, s);
+    else launch3d<P, 3>(g, op, ep, mode, dot, x, y, s);
   }
-  k_op3d<P, T2_3D, T3_3D><<<g.grid, Sh::NT, Sh::SMEM, s>>>(op, ep, mode, dot, x, y, g.chunk);
 }
 
-int launch_operator(Handle& h, int level, const double* x, double* out, EpiMode mode, DotMode dot, const Epi& epi,
-                    cudaStream_t s) {
-  const Level& L = h.lv[level];
+int launch_operator(Handle& h, int sy, int level, const double* x, double* out, EpiMode mode, DotMode dot,
+                    const Epi& epi, cudaStream_t s) {
+  const System& S = h.sys[sy];
+  const OpParams& op = S.lv[level].op;
   Grid g = grid_for(h, level);
   const int nct = g.grid.x * g.grid.y * g.grid.z;
   if (dot != DOT_NONE && (size_t)nct > h.partial_len) throw Error{IGACD_E_ARG, "partial buffer too small"};
-  if (h.dim == 2) {
-    switch (h.p) {
-      case 1: launch2d<1>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 2: launch2d<2>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 3: launch2d<3>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 4: launch2d<4>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 5: launch2d<5>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 6: launch2d<6>(g, L.op, epi, mode, dot, x, out, s); break;
-      default: throw Error{IGACD_E_ARG, "degree out of range"};
-    }
-  } else {
-    switch (h.p) {
-      case 1: launch3d<1>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 2: launch3d<2>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 3: launch3d<3>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 4: launch3d<4>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 5: launch3d<5>(g, L.op, epi, mode, dot, x, out, s); break;
-      case 6: launch3d<6>(g, L.op, epi, mode, dot, x, out, s); break;
-      default: throw Error{IGACD_E_ARG, "degree out of range"};
-    }
+  switch (h.p) {
+    case 1: dispatch<1>(h.dim, S.nc, g, op, epi, mode, dot, x, out, s); break;
+    case 2: dispatch<2>(h.dim, S.nc, g, op, epi, mode, dot, x, out, s); break;
+    case 3: dispatch<3>(h.dim, S.nc, g, op, epi, mode, dot, x, out, s); break;
+    case 4: dispatch<4>(h.dim, S.nc, g, op, epi, mode, dot, x, out, s); break;
+    case 5: dispatch<5>(h.dim, S.nc, g, op, epi, mode, dot, x, out, s); break;
+    case 6: dispatch<6>(h.dim, S.nc, g, op, epi, mode, dot, x, out, s); break;
+    default: throw Error{IGACD_E_ARG, "degree out of range"};
   }
   IGACD_LAUNCH_CHECK();
   count_launch(h);

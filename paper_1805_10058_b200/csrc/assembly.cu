@@ -11,6 +11,7 @@
 // column j = coefficients of the coarse B-spline N^c_j in the fine basis, by the Oslo
 // recurrence (Cohen-Lyche-Riesenfeld) -- one thread per entry.
 #include <cmath>
+#include <cstring>
 
 #include "internal.cuh"
 
@@ -174,7 +175,7 @@ void assemble_level(Handle& h, Level& L, cudaStream_t s) {
   }
   IGACD_CUDA(cudaStreamSynchronize(s));
   // Toeplitz rows: 2p-1 <= k <= m-2p (all band columns are cardinal B-splines)
-  OpParams& op = L.op;
+  OpParams& op = L.geo;
   op.m = m;
   op.bM = L.band[0];
   op.bA = L.band[1];
@@ -194,7 +195,7 @@ void assemble_level(Handle& h, Level& L, cudaStream_t s) {
       op.tS[o] = L.hband[2][(size_t)k * W + o + p];
     }
   }
-  op.c = h.coef;
+  std::memset(&op.c, 0, sizeof(op.c));
 }
 
 void build_transfer(Handle& h, int p, int nc, Transfer1D& T, cudaStream_t s) {

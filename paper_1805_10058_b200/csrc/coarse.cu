@@ -20,7 +20,7 @@ __global__ void k_dense_coarse(OpParams op, int dim, int p, double* A, int N) {
   if (idx >= (long long)N * N) return;
   const int I = (int)(idx / N), J = (int)(idx % N);
   const int m = op.m;
-  const int ns = dim == 2 ? m * m : m * m * m;
+  const int ns = dim == 2 ? m * m : m * m * m;   // N = nc * ns
   const int i = I / ns, j = J / ns;
   int kI[3] = {0, 0, 0}, kJ[3] = {0, 0, 0};
   int fi = I % ns, fj = J % ns;
@@ -93,14 +93,16 @@ __global__ void k_dense_matvec(const double* __restrict__ A, const double* __res
   if (lane == 0) x[warp] = s;
 }
 
-void build_coarse_inverse(Handle& h, cudaStream_t s) {
-  Level& L = h.lv.back();
+void build_coarse_inverse(Handle& h, int sy, cudaStream_t s) {
+  System& S = h.sys[sy];
+  SysLevel& L = S.lv.back();
   const int N = (int)L.ndof;
-  IGACD_CUDA(cudaMalloc(&h.cinv, sizeof(double) * (size_t)N * N));
+  IGACD_CUDA(cudaMalloc(&S.cinv, sizeof(double) * (size_t)N * N));
+  double* cinv = S.cinv;
   const long long NN = (long long)N * N;
   const int bs = 256;
   const unsigned gb = (unsigned)((NN + bs - 1) / bs);
-  k_dense_coarse<<<gb, bs, 0, s>>>(L.op, h.dim, h.p, h.cinv, N);
+  k_dense_coarse<<<gb, bs, 0, s>>>(L.op, h.dim, h.p, cinv, N);
   IGACD_LAUNCH_CHECK();
   count_launch(h);
   double *row, *col;
@@ -110,13 +112,13 @@ void build_coarse_inverse(Handle& h, cudaStream_t s) {
   IGACD_CUDA(cudaMalloc(&bad, sizeof(int)));
   IGACD_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   for (int k = 0; k < N; ++k) {
-    k_sweep_save<<<(N + bs - 1) / bs, bs, 0, s>>>(h.cinv, N, k, row, col, bad);
-    k_sweep_apply<<<gb, bs, 0, s>>>(h.cinv, N, k, row, col);
+    k_sweep_save<<<(N + bs - 1) / bs, bs, 0, s>>>(cinv, N, k, row, col, bad);
+    k_sweep_apply<<<gb, bs, 0, s>>>(cinv, N, k, row, col);
     count_launch(h);
     count_launch(h);
   }
   IGACD_LAUNCH_CHECK();
-  k_negate_sym<<<gb, bs, 0, s>>>(h.cinv, N);
+  k_negate_sym<<<gb, bs, 0, s>>>(cinv, N);
   IGACD_LAUNCH_CHECK();
   count_launch(h);
   int hbad = 0;
@@ -128,10 +130,11 @@ void build_coarse_inverse(Handle& h, cudaStream_t s) {
   if (hbad) throw Error{IGACD_E_NOTSPD, "coarsest-level matrix is not positive definite"};
 }
 
-void launch_coarse_solve(Handle& h, const double* b, double* x, cudaStream_t s) {
-  const int N = (int)h.lv.back().ndof;
+void launch_coarse_solve(Handle& h, int sy, const double* b, double* x, cudaStream_t s) {
+  const System& S = h.sys[sy];
+  const int N = (int)S.lv.back().ndof;
   const int bs = 256;
-  k_dense_matvec<<<(N * 32 + bs - 1) / bs, bs, 0, s>>>(h.cinv, b, x, N);
+  k_dense_matvec<<<(N * 32 + bs - 1) / bs, bs, 0, s>>>(S.cinv, b, x, N);
   IGACD_LAUNCH_CHECK();
   count_launch(h);
 }

@@ -58,28 +58,46 @@ struct Transfer1D {   // 1D prolongation P (m_f x m_c) in fixed-width row storag
   std::vector<double> hdense;   // host dense copy (debug/parity)
 };
 
+// Geometry of one level (shared by the vector system and the auxiliary scalar system).
 struct Level {
   int n = 0, m = 0;
-  size_t nscal = 0, ndof = 0;
+  size_t nscal = 0;
   double* band[3] = {nullptr, nullptr, nullptr};  // M, A, S
   std::vector<double> hband[3];
-  OpParams op;
+  OpParams geo;  // m, zones, bands, Toeplitz rows (coefficients filled per system)
+};
+
+// Per-level state of one system.
+struct SysLevel {
+  OpParams op;         // geometry of the level + this system's pattern coefficients
+  size_t ndof = 0;
   double rho = 0.0, omega = 0.0;
-  // work vectors (ndof each)
-  double* b = nullptr;
+  double* b = nullptr;  // work vectors (ndof each)
   double* x = nullptr;
   double* t = nullptr;
   double* r = nullptr;
 };
 
+// A linear system on the level hierarchy: the d-component operator A (nc = d) or the
+// auxiliary scalar operator A_s = Pi^T A Pi on span{b0 s} (nc = 1), reading R8.
+struct System {
+  int nc = 0;
+  Coef coef;
+  std::vector<SysLevel> lv;
+  double* cinv = nullptr;   // dense inverse of the coarsest level
+};
+
+enum Precond { PRECOND_VCYCLE = 0, PRECOND_AUX = 1 };
+
 struct Handle {
   int dim = 0, p = 0;
   int nu_pre = 1, nu_post = 1;
-  Coef coef;
+  double b0[3] = {0, 0, 0};
   std::vector<Level> lv;
   std::vector<Transfer1D> tr;   // tr[l]: level l+1 -> level l
-  // coarsest level exact inverse (dense, ndof_L x ndof_L)
-  double* cinv = nullptr;
+  System sys[2];                // 0: vector operator, 1: auxiliary scalar operator
+  bool has_aux = false;
+  int precond = PRECOND_VCYCLE;
   // transfer scratch (max size), reductions
   double* scratch0 = nullptr;
   double* scratch1 = nullptr;
@@ -88,14 +106,14 @@ struct Handle {
   size_t partial_len = 0;
   double* scal = nullptr;       // device scalars
   double* hscal = nullptr;      // pinned host mirror
-  // PCG vectors (level-0 size)
+  // PCG / preconditioner vectors (level-0 size)
   double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *px = nullptr, *pb = nullptr;
+  double *aw = nullptr, *ar = nullptr;   // aux preconditioner work (level-0 vector size)
   cudaStream_t stream = nullptr;
   // instrumentation
   long long launches = 0, apply_launches = 0;
   double apply_ms = 0.0;
   bool profiling = false;
-  std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
 };
 
@@ -121,28 +139,33 @@ void build_transfer(Handle& h, int p, int n_coarse, Transfer1D& T, cudaStream_t 
 void gauss_legendre(int q, double* x01, double* w01);
 
 // ---- apply.cu -----------------------------------------------------------------------
-// out = epilogue(A x); returns number of CTAs that wrote partial sums (0 if dot == DOT_NONE)
-int launch_operator(Handle& h, int level, const double* x, double* out, EpiMode mode, DotMode dot,
+// out = epilogue(A x) for system `sy`; returns the number of CTAs that wrote partial sums
+// (0 if dot == DOT_NONE)
+int launch_operator(Handle& h, int sy, int level, const double* x, double* out, EpiMode mode, DotMode dot,
                     const Epi& epi, cudaStream_t s);
 int operator_ctas(const Handle& h, int level);
 
 // ---- transfer.cu --------------------------------------------------------------------
-void launch_prolong(Handle& h, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s);
-void launch_restrict(Handle& h, int level, const double* xf, double* xc, cudaStream_t s);
+void launch_prolong(Handle& h, int nc, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s);
+void launch_restrict(Handle& h, int nc, int level, const double* xf, double* xc, cudaStream_t s);
+// auxiliary-space maps: s = Pi^T v = sum_j b0_j v_j;  v (+)= Pi s = b0 s
+void launch_pi_t(Handle& h, const double* v, double* sc, cudaStream_t s);
+void launch_pi(Handle& h, const double* sc, double* v, bool accumulate, cudaStream_t s);
 
 // ---- coarse.cu ----------------------------------------------------------------------
-void build_coarse_inverse(Handle& h, cudaStream_t s);
-void launch_coarse_solve(Handle& h, const double* b, double* x, cudaStream_t s);
+void build_coarse_inverse(Handle& h, int sy, cudaStream_t s);
+void launch_coarse_solve(Handle& h, int sy, const double* b, double* x, cudaStream_t s);
 
 // ---- vec.cu -------------------------------------------------------------------------
 int vec_ctas(size_t n);
 void launch_dot(Handle& h, const double* a, const double* b, size_t n, double* partial, cudaStream_t s);
 void launch_finalize(Handle& h, const double* partial, int nparts, double* dst, cudaStream_t s);
-void launch_scale_dinv(Handle& h, int level, const double* b, double* x, double omega, cudaStream_t s);
+void launch_scale_dinv(Handle& h, int sy, int level, const double* b, double* x, double omega, cudaStream_t s);
 void launch_copy(Handle& h, const double* a, double* b, size_t n, cudaStream_t s);
 void launch_zero(Handle& h, double* a, size_t n, cudaStream_t s);
+void launch_axpy_inplace(Handle& h, const double* a, double* b, size_t n, cudaStream_t s);   // b += a
 void launch_scale(Handle& h, double* a, const double* scal_num, const double* scal_den, size_t n, cudaStream_t s);
-void launch_dvdot(Handle& h, int level, const double* v, double* partial, cudaStream_t s);
+void launch_dvdot(Handle& h, int sy, int level, const double* v, double* partial, cudaStream_t s);
 void launch_hash_vector(Handle& h, double* v, size_t n, cudaStream_t s);
 // PCG fused updates (scalars on device: scal[...])
 void launch_pcg_update_xr(Handle& h, double* x, double* r, const double* p, const double* q, size_t n,

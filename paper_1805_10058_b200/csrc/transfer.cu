@@ -42,9 +42,9 @@ static void axis_pass(Handle& h, const double* in, double* out, long long outer,
 }
 
 // level l (fine, m_f) <- level l+1 (coarse, m_c)
-void launch_prolong(Handle& h, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s) {
+void launch_prolong(Handle& h, int nc, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s) {
   const Transfer1D& T = h.tr[level];
-  const long long d = h.dim, mf = T.mf, mc = T.mc;
+  const long long d = nc, mf = T.mf, mc = T.mc;
   if (h.dim == 2) {
     // [d][mc][mc] -> [d][mc][mf] -> [d][mf][mf]
     axis_pass(h, xc, h.scratch0, d * mc, (int)mc, (int)mf, 1, T.p_start, T.p_w, T.wp, false, s);
@@ -56,9 +56,9 @@ void launch_prolong(Handle& h, int level, const double* xc, double* xf, bool acc
   }
 }
 
-void launch_restrict(Handle& h, int level, const double* xf, double* xc, cudaStream_t s) {
+void launch_restrict(Handle& h, int nc, int level, const double* xf, double* xc, cudaStream_t s) {
   const Transfer1D& T = h.tr[level];
-  const long long d = h.dim, mf = T.mf, mc = T.mc;
+  const long long d = nc, mf = T.mf, mc = T.mc;
   if (h.dim == 2) {
     // [d][mf][mf] -> [d][mc][mf] -> [d][mc][mc]
     axis_pass(h, xf, h.scratch0, d, (int)mf, (int)mc, mf, T.r_start, T.r_w, T.wr, false, s);
@@ -68,6 +68,54 @@ void launch_restrict(Handle& h, int level, const double* xf, double* xc, cudaStr
     axis_pass(h, h.scratch0, h.scratch1, d * mc, (int)mf, (int)mc, mf, T.r_start, T.r_w, T.wr, false, s);
     axis_pass(h, h.scratch1, xc, d * mc * mc, (int)mf, (int)mc, 1, T.r_start, T.r_w, T.wr, false, s);
   }
+}
+
+// Auxiliary-space maps of reading R8: Pi s = b0 s (component j = b0_j s), Pi^T v = sum_j b0_j v_j.
+struct B0 {
+  double b[3];
+};
+
+__global__ void k_pi_t(const double* __restrict__ v, double* __restrict__ sc, size_t ns, int d, B0 b0) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ns; i += (size_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < d; ++j) acc = fma(b0.b[j], v[j * ns + i], acc);
+    sc[i] = acc;
+  }
+}
+
+__global__ void k_pi(const double* __restrict__ sc, double* __restrict__ v, size_t ns, int d, B0 b0, int accumulate) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ns; i += (size_t)gridDim.x * blockDim.x) {
+    const double si = sc[i];
+    for (int j = 0; j < d; ++j) {
+      const double val = b0.b[j] * si;
+      if (accumulate) v[j * ns + i] += val;
+      else v[j * ns + i] = val;
+    }
+  }
+}
+
+static int grid1d(size_t n) {
+  long long b = (long long)((n + 255) / 256);
+  if (b > 148 * 8) b = 148 * 8;
+  return (int)(b < 1 ? 1 : b);
+}
+
+void launch_pi_t(Handle& h, const double* v, double* sc, cudaStream_t s) {
+  B0 b0;
+  for (int j = 0; j < 3; ++j) b0.b[j] = h.b0[j];
+  const size_t ns = h.lv[0].nscal;
+  k_pi_t<<<grid1d(ns), 256, 0, s>>>(v, sc, ns, h.dim, b0);
+  IGACD_LAUNCH_CHECK();
+  count_launch(h);
+}
+
+void launch_pi(Handle& h, const double* sc, double* v, bool accumulate, cudaStream_t s) {
+  B0 b0;
+  for (int j = 0; j < 3; ++j) b0.b[j] = h.b0[j];
+  const size_t ns = h.lv[0].nscal;
+  k_pi<<<grid1d(ns), 256, 0, s>>>(sc, v, ns, h.dim, b0, accumulate ? 1 : 0);
+  IGACD_LAUNCH_CHECK();
+  count_launch(h);
 }
 
 }  // namespace igacd

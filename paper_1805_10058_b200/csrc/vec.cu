@@ -62,7 +62,7 @@ __device__ __forceinline__ double diag_at(const OpParams& op, int p, size_t gidx
   const int m = op.m;
   const int W = 2 * p + 1;
   const size_t ns = DIM == 2 ? (size_t)m * m : (size_t)m * m * m;
-  const int i = (int)(gidx / ns);
+  const int i = (int)(gidx / ns);   // component (0 for the scalar system)
   size_t f = gidx % ns;
   int k[3] = {0, 0, 0};
 #pragma unroll
@@ -122,6 +122,10 @@ __global__ void k_pcg_xr(double* __restrict__ x, double* __restrict__ r, const d
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
+__global__ void k_axpy1(const double* __restrict__ a, double* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)VBS + threadIdx.x; i < n; i += (size_t)gridDim.x * VBS) b[i] += a[i];
+}
+
 // beta = rz_new/rz_old;  p = z + beta p
 __global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ z, size_t n, const double* rzn,
                         const double* rzo) {
@@ -146,6 +150,10 @@ void launch_copy(Handle& h, const double* a, double* b, size_t n, cudaStream_t s
   k_copy<<<vec_ctas(n), VBS, 0, s>>>(a, b, n);
   LAUNCH_TAIL();
 }
+void launch_axpy_inplace(Handle& h, const double* a, double* b, size_t n, cudaStream_t s) {
+  k_axpy1<<<vec_ctas(n), VBS, 0, s>>>(a, b, n);
+  LAUNCH_TAIL();
+}
 void launch_zero(Handle& h, double* a, size_t n, cudaStream_t s) {
   k_zero<<<vec_ctas(n), VBS, 0, s>>>(a, n);
   LAUNCH_TAIL();
@@ -154,14 +162,14 @@ void launch_scale(Handle& h, double* a, const double* sq, const double*, size_t 
   k_normalize<<<vec_ctas(n), VBS, 0, s>>>(a, sq, n);
   LAUNCH_TAIL();
 }
-void launch_scale_dinv(Handle& h, int level, const double* b, double* x, double omega, cudaStream_t s) {
-  const Level& L = h.lv[level];
+void launch_scale_dinv(Handle& h, int sy, int level, const double* b, double* x, double omega, cudaStream_t s) {
+  const SysLevel& L = h.sys[sy].lv[level];
   if (h.dim == 2) k_scale_dinv<2><<<vec_ctas(L.ndof), VBS, 0, s>>>(L.op, h.p, b, x, omega, L.ndof);
   else k_scale_dinv<3><<<vec_ctas(L.ndof), VBS, 0, s>>>(L.op, h.p, b, x, omega, L.ndof);
   LAUNCH_TAIL();
 }
-void launch_dvdot(Handle& h, int level, const double* v, double* partial, cudaStream_t s) {
-  const Level& L = h.lv[level];
+void launch_dvdot(Handle& h, int sy, int level, const double* v, double* partial, cudaStream_t s) {
+  const SysLevel& L = h.sys[sy].lv[level];
   if (h.dim == 2) k_dvdot<2><<<vec_ctas(L.ndof), VBS, 0, s>>>(L.op, h.p, v, L.ndof, partial);
   else k_dvdot<3><<<vec_ctas(L.ndof), VBS, 0, s>>>(L.op, h.p, v, L.ndof, partial);
   LAUNCH_TAIL();

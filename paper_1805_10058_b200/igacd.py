@@ -45,6 +45,11 @@ _smooth = _sig("igacd_smooth", [_vp, _c_int, _vp, _vp, _c_int, _c_double, _vp])
 _restrict = _sig("igacd_restrict", [_vp, _c_int, _vp, _vp, _vp])
 _prolong = _sig("igacd_prolong", [_vp, _c_int, _vp, _vp, _c_int, _vp])
 _vcycle = _sig("igacd_vcycle", [_vp, _vp, _vp, _vp])
+_precond = _sig("igacd_precond", [_vp, _vp, _vp, _vp])
+_set_precond = _sig("igacd_set_preconditioner", [_vp, _c_int])
+_get_precond = _sig("igacd_get_preconditioner", [_vp, _P(_c_int)])
+_apply_aux = _sig("igacd_apply_aux", [_vp, _c_int, _vp, _vp, _vp])
+_aux_omega = _sig("igacd_aux_omega", [_vp, _c_int, _P(_c_double), _P(_c_double)])
 _solve = _sig("igacd_solve", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
 _solve_host = _sig("igacd_solve_host", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
 _get_band = _sig("igacd_get_band", [_vp, _c_int, _c_int, _P(_c_double)])
@@ -54,6 +59,8 @@ _get_prof = _sig("igacd_get_profile", [_vp, _P(ctypes.c_longlong), _P(ctypes.c_l
 _reset_prof = _sig("igacd_reset_profile", [_vp])
 
 IGACD_E_NOCONV = -4
+IGACD_PRECOND_VCYCLE = 0
+IGACD_PRECOND_AUX = 1
 
 
 class IgacdError(RuntimeError):
@@ -162,6 +169,30 @@ def igacd_prolong(h, level, x_coarse, x_fine, accumulate=False, stream=None):
 
 def igacd_vcycle(h, b, x, stream=None):
     _check(_vcycle(h, _dptr(b), _dptr(x), _stream(stream)))
+
+
+def igacd_precond(h, b, x, stream=None):
+    _check(_precond(h, _dptr(b), _dptr(x), _stream(stream)))
+
+
+def igacd_set_preconditioner(h, mode):
+    _check(_set_precond(h, mode))
+
+
+def igacd_get_preconditioner(h):
+    v = _c_int()
+    _check(_get_precond(h, ctypes.byref(v)))
+    return v.value
+
+
+def igacd_apply_aux(h, level, s_in, s_out, stream=None):
+    _check(_apply_aux(h, level, _dptr(s_in), _dptr(s_out), _stream(stream)))
+
+
+def igacd_aux_omega(h, level):
+    w, r = _c_double(), _c_double()
+    _check(_aux_omega(h, level, ctypes.byref(w), ctypes.byref(r)))
+    return w.value, r.value
 
 
 def igacd_solve(h, b, x, tol, maxit, stream=None, raise_on_noconv=True):

@@ -11,7 +11,7 @@ import pytest
 import inputs
 from oracle import matrices1d as m1
 from oracle.krylov import pcg
-from oracle.multigrid import Hierarchy
+from oracle.multigrid import AuxPreconditioner, Hierarchy, aux_map
 from oracle.operator import Discretization, form_alfven, form_curldiv
 from oracle.transfer import prolongation, prolongation_1d
 
@@ -224,8 +224,44 @@ def test_vcycle_matches_oracle(case):
         ig.igacd_destroy(h)
 
 
+@pytest.mark.parametrize("case", [Case(2, 3, 24, levels=2), Case(3, 2, 6, levels=2), Case(3, 4, 9)], ids=repr)
+def test_aux_operator_matches_oracle(case):
+    h = case.handle()
+    try:
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        Pi = aux_map(case.d, disc.nscal, case.b0)
+        As = Pi.T @ A @ Pi
+        s = np.random.default_rng(2).standard_normal(disc.nscal)
+        y = torch.zeros(disc.nscal, dtype=torch.float64, device="cuda")
+        ig.igacd_apply_aux(h, 0, to_dev(s), y)
+        assert_close(to_host(y), As @ s, 1e-12, "A_s")
+    finally:
+        ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("case", VCYCLE_CASES[:4], ids=repr)
+def test_aux_preconditioner_matches_oracle(case):
+    h = case.handle()
+    try:
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels)
+        assert ig.igacd_get_preconditioner(h) == ig.IGACD_PRECOND_AUX
+        for l in range(len(B.Vs.ns) - 1):
+            w, rho = ig.igacd_aux_omega(h, l)
+            assert abs(rho - B.Vs.rho[l]) <= 1e-10 * B.Vs.rho[l]
+        b = np.random.default_rng(13).uniform(-1, 1, disc.ndof)
+        x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        ig.igacd_precond(h, to_dev(b), x)
+        assert_close(to_host(x), B(b), 1e-12, "aux precond")
+    finally:
+        ig.igacd_destroy(h)
+
+
 SOLVE_CASES = [Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels=2),
-               Case(2, 3, 32, nu=1.0, beta=0.1, levels=0), Case(3, 2, 8, nu=1.0, beta=0.1, levels=2)]
+               Case(2, 3, 32, nu=1.0, beta=0.1, levels=0), Case(3, 2, 8, nu=1.0, beta=0.1, levels=2),
+               Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2))]
 
 
 @pytest.mark.parametrize("case", SOLVE_CASES, ids=repr)
@@ -234,9 +270,9 @@ def test_solve_matches_oracle(case):
     try:
         disc = Discretization(case.d, case.p, case.n)
         A = disc.assemble(case.form)
-        H = Hierarchy(A, case.d, case.p, case.n, case.levels)
+        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels)
         b = np.random.default_rng(5).uniform(-1, 1, disc.ndof)
-        xo, ito, hist = pcg(A, b, H.vcycle, 1e-8, 2000)
+        xo, ito, hist = pcg(A, b, B, 1e-8, 2000)
         x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
         it, rel = ig.igacd_solve(h, to_dev(b), x, 1e-8, 2000)
         xg = to_host(x)
@@ -244,6 +280,24 @@ def test_solve_matches_oracle(case):
         assert rel < 1e-8
         assert np.linalg.norm(b - A @ xg) / np.linalg.norm(b) < 1e-8 * 1.5
         assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-8
+    finally:
+        ig.igacd_destroy(h)
+
+
+def test_plain_vcycle_preconditioner_solve():
+    case = Case(2, 3, 32, nu=1.0, beta=0.1, levels=0)
+    h = case.handle()
+    try:
+        ig.igacd_set_preconditioner(h, ig.IGACD_PRECOND_VCYCLE)
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        H = Hierarchy(A, case.d, case.p, case.n, case.levels)
+        b = np.random.default_rng(5).uniform(-1, 1, disc.ndof)
+        xo, ito, hist = pcg(A, b, H.vcycle, 1e-8, 2000)
+        x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        it, rel = ig.igacd_solve(h, to_dev(b), x, 1e-8, 2000)
+        assert abs(it - ito) <= 1 and rel < 1e-8
+        assert np.linalg.norm(to_host(x) - xo) / np.linalg.norm(xo) <= 1e-8
     finally:
         ig.igacd_destroy(h)
 
