@@ -102,16 +102,16 @@ def cpu_sample(cfg):
     """The oracle (as it stands) on a bounded sample of the workload: the same operator
     parameters and degree on a reduced mesh; returns (DOF/s, seconds, description)."""
     from oracle.krylov import pcg
-    from oracle.multigrid import Hierarchy
+    from oracle.multigrid import AuxPreconditioner
     from oracle.operator import Discretization, form_alfven
-    n = 8 if cfg.dim == 3 else 32
+    n = 4 if cfg.dim == 3 else 32
     small = cfg.with_(n=n, levels=0)
     t0 = time.perf_counter()
     disc = Discretization(small.dim, small.p, small.n)
     A = disc.assemble(form_alfven(small.nu, small.beta, small.lam, small.b0))
-    H = Hierarchy(A, small.dim, small.p, small.n, small.levels)
+    B = AuxPreconditioner(A, small.dim, small.p, small.n, small.b0, small.levels)
     b = inputs.rhs(small)
-    _, it, hist = pcg(A, b, H.vcycle, small.tol, 5000)
+    _, it, hist = pcg(A, b, B, small.tol, 5000)
     dt = time.perf_counter() - t0
     desc = ("oracle assemble + Galerkin hierarchy + PCG/V-cycle solve of %s with n=%d (%d DOFs, %d iterations, "
             "rel.res %.1e)" % (cfg.name, n, small.ndof, it, hist[-1]))

@@ -17,6 +17,35 @@
 
 namespace igacd {
 
+// 8-byte asynchronous global->shared copy (LDGSTS); src_bytes = 0 zero-fills the slot.
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc, bool valid) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int nbytes = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(nbytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------------------------------
+// Marching-direction weights: column s of each 1D factor, F[t][s] for t = s-p..s+p,
+// zero outside the CTA's output chunk [c0, c1).  Written one slab ahead into shared memory.
+// ---------------------------------------------------------------------------------------
+template <int P>
+__device__ __forceinline__ void load_col_weights(const OpParams& op, int s, int c0, int c1, double* w) {
+  constexpr int R = 2 * P + 1;
+  const int tid = threadIdx.x;
+  if (tid < 3 * R) {
+    const int f = tid / R, o = tid % R - P;
+    const int t = s + o;
+    double v = 0.0;
+    if (t >= c0 && t < c1) {
+      const double* band = f == 0 ? op.bM : (f == 1 ? op.bS : op.bA);
+      v = __ldg(band + (size_t)t * R + P - o);   // F[t][s], s - t = -o
+    }
+    w[tid] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // 2D
 // ---------------------------------------------------------------------------------------
@@ -28,6 +57,7 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
   constexpr int W = NT + 2 * P;
   constexpr int LPT = (W + NT - 1) / NT;
   __shared__ double xs[2][NC][W];
+  __shared__ double wts[2][3 * R];
   __shared__ double red[NT / 32];
   const int m = op.m;
   const size_t ms = (size_t)m * m;
@@ -47,135 +77,125 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[i][r] = 0.0;
   double dsum = 0.0;
-  double pre[NC][LPT];
 
-  auto gload = [&](int s) {
+  // slab s -> xs[buf] by asynchronous copies (zero fill outside the domain)
+  auto prefetch = [&](int s, int buf) {
 #pragma unroll
     for (int j = 0; j < NC; ++j)
 #pragma unroll
       for (int i = 0; i < LPT; ++i) {
         const int idx = tid + i * NT;
         const int col = t0 - P + idx;
-        double v = 0.0;
-        if (idx < W && s < m && col >= 0 && col < m) v = __ldg(x + j * ms + (size_t)s * m + col);
-        pre[j][i] = v;
+        if (idx < W) {
+          const bool ok = s < m && col >= 0 && col < m;
+          cp_async8(&xs[buf][j][idx], ok ? x + j * ms + (size_t)s * m + col : x, ok);
+        }
       }
-  };
-  auto sstore = [&](int buf) {
-#pragma unroll
-    for (int j = 0; j < NC; ++j)
-#pragma unroll
-      for (int i = 0; i < LPT; ++i) {
-        const int idx = tid + i * NT;
-        if (idx < W) xs[buf][j][idx] = pre[j][i];
-      }
+    cp_async_commit();
   };
 
-  gload(sb);
-  sstore(0);
+  prefetch(sb, 0);
+  load_col_weights<P>(op, sb, c0, c1, wts[0]);
+  cp_async_wait_all();
   __syncthreads();
-  for (int g = sb; g < se; g += R) {
+#pragma unroll 1
+  for (int s = sb; s < se; ++s) {
+    const int buf = (s - sb) & 1;
+    const bool more = s + 1 < se;
+    if (more) {
+      prefetch(s + 1, buf ^ 1);
+      load_col_weights<P>(op, s + 1, c0, c1, wts[buf ^ 1]);
+    }
+    if (s < m) {
+      double zM[NC], zS[NC], zA[NC];
+      {
+        double uM[NC], uS[NC], uA[NC];
 #pragma unroll
-    for (int ph = 0; ph < R; ++ph) {
-      const int s = g + ph;
-      if (s < se) {
-        const int buf = (s - sb) & 1;
-        const bool more = s + 1 < se;
-        if (more) gload(s + 1);
-        if (s < m) {
-          double zM[NC], zS[NC], zA[NC];
-          {
-            double uM[NC], uS[NC], uA[NC];
+        for (int j = 0; j < NC; ++j) {
+          const double* xr = &xs[buf][j][tid + P];
+          const double xc = xr[0];
+          double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
 #pragma unroll
-            for (int j = 0; j < NC; ++j) {
-              const double* xr = &xs[buf][j][tid + P];
-              const double xc = xr[0];
-              double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
+          for (int o = 1; o <= P; ++o) {
+            const double lo = xr[-o], hi = xr[o];
+            const double sp = lo + hi, sm = hi - lo;
+            vm = fma(op.tM[o], sp, vm);
+            vs = fma(op.tS[o], sp, vs);
+            va = fma(op.tA[o], sm, va);
+          }
+          if (zone) {
+            const double* rM = op.bM + (size_t)k * R + P;
+            const double* rS = op.bS + (size_t)k * R + P;
+            const double* rA = op.bA + (size_t)k * R + P;
+            vm = vs = va = 0.0;
 #pragma unroll
-              for (int o = 1; o <= P; ++o) {
-                const double lo = xr[-o], hi = xr[o];
-                const double sp = lo + hi, sm = hi - lo;
-                vm = fma(op.tM[o], sp, vm);
-                vs = fma(op.tS[o], sp, vs);
-                va = fma(op.tA[o], sm, va);
-              }
-              if (zone) {
-                const double* rM = op.bM + (size_t)k * R + P;
-                const double* rS = op.bS + (size_t)k * R + P;
-                const double* rA = op.bA + (size_t)k * R + P;
-                vm = vs = va = 0.0;
-#pragma unroll
-                for (int o = -P; o <= P; ++o) {
-                  const double v = xr[o];
-                  vm = fma(__ldg(rM + o), v, vm);
-                  vs = fma(__ldg(rS + o), v, vs);
-                  va = fma(__ldg(rA + o), v, va);
-                }
-              }
-              uM[j] = vm;
-              uS[j] = vs;
-              uA[j] = va;
-            }
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-              zM[i] = zS[i] = zA[i] = 0.0;
-#pragma unroll
-              for (int j = 0; j < NC; ++j) {
-                zM[i] = fma(op.c.mass[i][j], uM[j], fma(op.c.S[1][i][j], uS[j], zM[i]));
-                zS[i] = fma(op.c.S[0][i][j], uM[j], zS[i]);
-                zA[i] = fma(op.c.AA[0][i][j], uA[j], zA[i]);
-              }
+            for (int o = -P; o <= P; ++o) {
+              const double v = xr[o];
+              vm = fma(__ldg(rM + o), v, vm);
+              vs = fma(__ldg(rS + o), v, vs);
+              va = fma(__ldg(rA + o), v, va);
             }
           }
+          uM[j] = vm;
+          uS[j] = vs;
+          uA[j] = va;
+        }
 #pragma unroll
-          for (int o = -P; o <= P; ++o) {
-            const int t = s + o;
-            if (t >= c0 && t < c1) {
-              const size_t wi = (size_t)t * R + P - o;   // F[t][s], s - t = -o
-              const double wM = __ldg(op.bM + wi), wS = __ldg(op.bS + wi), wA = __ldg(op.bA + wi);
-              const int slot = (ph + o + R) % R;
+        for (int i = 0; i < NC; ++i) {
+          zM[i] = zS[i] = zA[i] = 0.0;
 #pragma unroll
-              for (int i = 0; i < NC; ++i) acc[i][slot] = fma(wM, zM[i], fma(wS, zS[i], fma(wA, zA[i], acc[i][slot])));
-            }
+          for (int j = 0; j < NC; ++j) {
+            zM[i] = fma(op.c.mass[i][j], uM[j], fma(op.c.S[1][i][j], uS[j], zM[i]));
+            zS[i] = fma(op.c.S[0][i][j], uM[j], zS[i]);
+            zA[i] = fma(op.c.AA[0][i][j], uA[j], zA[i]);
           }
         }
-        {
-          const int t = s - P;
-          const int slot = (ph + R - P) % R;
-          if (t >= c0 && t < c1 && active) {
-            const size_t pt = (size_t)t * m + k;
-            double Dv[NC];
+      }
+      const double* w = wts[buf];
 #pragma unroll
-            for (int i = 0; i < NC; ++i) Dv[i] = 1.0;
-            if (mode >= EPI_JACOBI) {
-              const double Mt = __ldg(op.bM + (size_t)t * R + P), St = __ldg(op.bS + (size_t)t * R + P);
-              const double Mk = __ldg(op.bM + (size_t)k * R + P), Sk = __ldg(op.bS + (size_t)k * R + P);
+      for (int r = 0; r < R; ++r) {
+        const double wM = w[r], wS = w[R + r], wA = w[2 * R + r];
 #pragma unroll
-              for (int i = 0; i < NC; ++i)
-                Dv[i] = op.c.mass[i][i] * Mt * Mk + op.c.S[0][i][i] * St * Mk + op.c.S[1][i][i] * Mt * Sk;
-            }
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-              const double a = acc[i][slot];
-              const double D = Dv[i];
-              const size_t gi = (size_t)i * ms + pt;
-              double out;
-              if (mode == EPI_APPLY) out = a;
-              else if (mode == EPI_RESID) out = ep.b[gi] - a;
-              else if (mode == EPI_JACOBI) out = x[gi] + ep.omega * (ep.b[gi] - a) / D;
-              else out = a / D;
-              y[gi] = out;
-              if (dot == DOT_X_OUT) dsum = fma(x[gi], out, dsum);
-              else if (dot == DOT_OUT_OUT) dsum = fma(out, out, dsum);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < NC; ++i) acc[i][slot] = 0.0;
-        }
-        if (more) sstore(buf ^ 1);
-        __syncthreads();
+        for (int i = 0; i < NC; ++i) acc[i][r] = fma(wM, zM[i], fma(wS, zS[i], fma(wA, zA[i], acc[i][r])));
       }
     }
+    {
+      const int t = s - P;   // final: all contributions s' in [t-p, t+p] are in acc[.][0]
+      if (t >= c0 && t < c1 && active) {
+        const size_t pt = (size_t)t * m + k;
+        double Dv[NC];
+#pragma unroll
+        for (int i = 0; i < NC; ++i) Dv[i] = 1.0;
+        if (mode >= EPI_JACOBI) {
+          const double Mt = __ldg(op.bM + (size_t)t * R + P), St = __ldg(op.bS + (size_t)t * R + P);
+          const double Mk = __ldg(op.bM + (size_t)k * R + P), Sk = __ldg(op.bS + (size_t)k * R + P);
+#pragma unroll
+          for (int i = 0; i < NC; ++i)
+            Dv[i] = op.c.mass[i][i] * Mt * Mk + op.c.S[0][i][i] * St * Mk + op.c.S[1][i][i] * Mt * Sk;
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          const double a = acc[i][0];
+          const size_t gi = (size_t)i * ms + pt;
+          double out;
+          if (mode == EPI_APPLY) out = a;
+          else if (mode == EPI_RESID) out = ep.b[gi] - a;
+          else if (mode == EPI_JACOBI) out = x[gi] + ep.omega * (ep.b[gi] - a) / Dv[i];
+          else out = a / Dv[i];
+          y[gi] = out;
+          if (dot == DOT_X_OUT) dsum = fma(x[gi], out, dsum);
+          else if (dot == DOT_OUT_OUT) dsum = fma(out, out, dsum);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+#pragma unroll
+        for (int r = 0; r < R - 1; ++r) acc[i][r] = acc[i][r + 1];
+        acc[i][R - 1] = 0.0;
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
   }
   if (dot != DOT_NONE) {
 #pragma unroll
@@ -201,12 +221,12 @@ struct Op3dShape {
   static constexpr int HC = T3 + 2 * P;
   static constexpr int XS = HR * HC;        // one component of one slab tile
   static constexpr int US = T2 * HC;        // one stage-A output array
-  static constexpr int SMEM = (2 * NC * XS + 3 * NC * US) * 8 + (NT / 32) * 8;
+  static constexpr int SMEM = (2 * NC * XS + 3 * NC * US + 2 * 3 * R) * 8 + (NT / 32) * 8;
   static constexpr int LPT = (NC * XS + NT - 1) / NT;
 };
 
 template <int P, int T2, int T3, int NC>
-__global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep, int mode, int dot,
+__global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi ep, int mode, int dot,
                                                  const double* __restrict__ x, double* __restrict__ y,
                                                  int chunk) {
   using Sh = Op3dShape<P, T2, T3, NC>;
@@ -214,7 +234,8 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
   extern __shared__ double smem[];
   double* xs = smem;                   // [2][NC][HR][HC]
   double* us = smem + 2 * NC * XS;     // [3][NC][T2][HC]: index (F*NC + j), F: 0 M, 1 S, 2 A
-  double* red = us + 3 * NC * US;
+  double* wts = us + 3 * NC * US;      // [2][3R]
+  double* red = wts + 2 * 3 * R;
   const int m = op.m;
   const size_t ms = (size_t)m * m;
   const size_t m3 = ms * m;
@@ -235,197 +256,189 @@ __global__ void __launch_bounds__(T2* T3) k_op3d(const OpParams op, const Epi ep
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[i][r] = 0.0;
   double dsum = 0.0;
-  double pre[LPT];
 
-  auto gload = [&](int s) {
+  // slab s -> xs[buf] by asynchronous copies (zero fill outside the domain)
+  auto prefetch = [&](int s, int buf) {
 #pragma unroll
     for (int i = 0; i < LPT; ++i) {
       const int idx = tid + i * NT;
-      double v = 0.0;
-      if (idx < NC * XS && s < m) {
+      if (idx < NC * XS) {
         const int j = idx / XS, rem = idx % XS;
         const int hr = rem / HC, hc = rem % HC;
         const int g1 = r0 - P + hr, g2 = q0 - P + hc;
-        if (g1 >= 0 && g1 < m && g2 >= 0 && g2 < m) v = __ldg(x + j * m3 + (size_t)s * ms + (size_t)g1 * m + g2);
+        const bool ok = s < m && g1 >= 0 && g1 < m && g2 >= 0 && g2 < m;
+        cp_async8(xs + buf * NC * XS + idx, ok ? x + j * m3 + (size_t)s * ms + (size_t)g1 * m + g2 : x, ok);
       }
-      pre[i] = v;
     }
-  };
-  auto sstore = [&](int buf) {
-#pragma unroll
-    for (int i = 0; i < LPT; ++i) {
-      const int idx = tid + i * NT;
-      if (idx < NC * XS) xs[buf * NC * XS + idx] = pre[i];
-    }
+    cp_async_commit();
   };
 
-  gload(sb);
-  sstore(0);
+  prefetch(sb, 0);
+  load_col_weights<P>(op, sb, c0, c1, wts);
+  cp_async_wait_all();
   __syncthreads();
-  for (int g = sb; g < se; g += R) {
+#pragma unroll 1
+  for (int s = sb; s < se; ++s) {
+    const int buf = (s - sb) & 1;
+    const bool more = s + 1 < se;
+    if (more) {
+      prefetch(s + 1, buf ^ 1);
+      load_col_weights<P>(op, s + 1, c0, c1, wts + (buf ^ 1) * 3 * R);
+    }
+    if (s < m) {
+      // ---- stage A: contract direction 1 for rows [0,T2) x halo columns [0,HC)
+#pragma unroll 1
+      for (int it = tid; it < T2 * HC; it += NT) {
+        const int r = it / HC, cc = it % HC;
+        const int g1 = r0 + r;
+        const bool zoneA = g1 < m && (g1 < op.zoneL || g1 >= op.zoneR);
 #pragma unroll
-    for (int ph = 0; ph < R; ++ph) {
-      const int s = g + ph;
-      if (s < se) {
-        const int buf = (s - sb) & 1;
-        const bool more = s + 1 < se;
-        if (more) gload(s + 1);
-        if (s < m) {
-          // ---- stage A: contract direction 1 for rows [0,T2) x halo columns [0,HC)
-          for (int it = tid; it < T2 * HC; it += NT) {
-            const int r = it / HC, cc = it % HC;
-            const int g1 = r0 + r;
-            const bool zoneA = g1 < m && (g1 < op.zoneL || g1 >= op.zoneR);
+        for (int j = 0; j < NC; ++j) {
+          const double* xc_ = xs + buf * NC * XS + j * XS + (r + P) * HC + cc;
+          const double xc = xc_[0];
+          double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
 #pragma unroll
-            for (int j = 0; j < NC; ++j) {
-              const double* xc_ = xs + buf * NC * XS + j * XS + (r + P) * HC + cc;
-              const double xc = xc_[0];
-              double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
+          for (int o = 1; o <= P; ++o) {
+            const double lo = xc_[-o * HC], hi = xc_[o * HC];
+            const double sp = lo + hi, sm = hi - lo;
+            vm = fma(op.tM[o], sp, vm);
+            vs = fma(op.tS[o], sp, vs);
+            va = fma(op.tA[o], sm, va);
+          }
+          if (zoneA) {
+            const double* rM = op.bM + (size_t)g1 * R + P;
+            const double* rS = op.bS + (size_t)g1 * R + P;
+            const double* rA = op.bA + (size_t)g1 * R + P;
+            vm = vs = va = 0.0;
 #pragma unroll
-              for (int o = 1; o <= P; ++o) {
-                const double lo = xc_[-o * HC], hi = xc_[o * HC];
-                const double sp = lo + hi, sm = hi - lo;
-                vm = fma(op.tM[o], sp, vm);
-                vs = fma(op.tS[o], sp, vs);
-                va = fma(op.tA[o], sm, va);
-              }
-              if (zoneA) {
-                const double* rM = op.bM + (size_t)g1 * R + P;
-                const double* rS = op.bS + (size_t)g1 * R + P;
-                const double* rA = op.bA + (size_t)g1 * R + P;
-                vm = vs = va = 0.0;
-#pragma unroll
-                for (int o = -P; o <= P; ++o) {
-                  const double v = xc_[o * HC];
-                  vm = fma(__ldg(rM + o), v, vm);
-                  vs = fma(__ldg(rS + o), v, vs);
-                  va = fma(__ldg(rA + o), v, va);
-                }
-              }
-              us[(0 * NC + j) * US + it] = vm;
-              us[(1 * NC + j) * US + it] = vs;
-              us[(2 * NC + j) * US + it] = va;
+            for (int o = -P; o <= P; ++o) {
+              const double v = xc_[o * HC];
+              vm = fma(__ldg(rM + o), v, vm);
+              vs = fma(__ldg(rS + o), v, vs);
+              va = fma(__ldg(rA + o), v, va);
             }
           }
-          __syncthreads();
-          // ---- stage B: contract direction 2, combine patterns into z_{i,F0}
-          double zM[NC], zS[NC], zA[NC];
+          us[(0 * NC + j) * US + it] = vm;
+          us[(1 * NC + j) * US + it] = vs;
+          us[(2 * NC + j) * US + it] = va;
+        }
+      }
+      __syncthreads();
+      // ---- stage B: contract direction 2, combine patterns into z_{i,F0}
+      double zM[NC], zS[NC], zA[NC];
 #pragma unroll
-          for (int i = 0; i < NC; ++i) zM[i] = zS[i] = zA[i] = 0.0;
+      for (int i = 0; i < NC; ++i) zM[i] = zS[i] = zA[i] = 0.0;
 #pragma unroll
-          for (int j = 0; j < NC; ++j) {
-            const double* uM = us + (0 * NC + j) * US + tr * HC + tc + P;
-            const double* uS = us + (1 * NC + j) * US + tr * HC + tc + P;
-            const double* uA = us + (2 * NC + j) * US + tr * HC + tc + P;
-            double vMM, vMS, vMA, vSM, vAM, vAA;
-            {
-              const double c = uM[0];
-              double a1 = op.tM[0] * c, a2 = op.tS[0] * c, a3 = 0.0;
+      for (int j = 0; j < NC; ++j) {
+        const double* uM = us + (0 * NC + j) * US + tr * HC + tc + P;
+        const double* uS = us + (1 * NC + j) * US + tr * HC + tc + P;
+        const double* uA = us + (2 * NC + j) * US + tr * HC + tc + P;
+        double vMM, vMS, vMA, vSM, vAM, vAA;
+        {
+          const double c = uM[0];
+          double a1 = op.tM[0] * c, a2 = op.tS[0] * c, a3 = 0.0;
 #pragma unroll
-              for (int o = 1; o <= P; ++o) {
-                const double lo = uM[-o], hi = uM[o];
-                const double sp = lo + hi, sm = hi - lo;
-                a1 = fma(op.tM[o], sp, a1);
-                a2 = fma(op.tS[o], sp, a2);
-                a3 = fma(op.tA[o], sm, a3);
-              }
-              vMM = a1; vMS = a2; vMA = a3;
-            }
-            {
-              double a1 = op.tM[0] * uS[0];
-#pragma unroll
-              for (int o = 1; o <= P; ++o) a1 = fma(op.tM[o], uS[-o] + uS[o], a1);
-              vSM = a1;
-            }
-            {
-              const double c = uA[0];
-              double a1 = op.tM[0] * c, a3 = 0.0;
-#pragma unroll
-              for (int o = 1; o <= P; ++o) {
-                const double lo = uA[-o], hi = uA[o];
-                a1 = fma(op.tM[o], lo + hi, a1);
-                a3 = fma(op.tA[o], hi - lo, a3);
-              }
-              vAM = a1; vAA = a3;
-            }
-            if (zoneB) {
-              const double* rM = op.bM + (size_t)gc * R + P;
-              const double* rS = op.bS + (size_t)gc * R + P;
-              const double* rA = op.bA + (size_t)gc * R + P;
-              vMM = vMS = vMA = vSM = vAM = vAA = 0.0;
-#pragma unroll
-              for (int o = -P; o <= P; ++o) {
-                const double wm = __ldg(rM + o), ws = __ldg(rS + o), wa = __ldg(rA + o);
-                vMM = fma(wm, uM[o], vMM);
-                vMS = fma(ws, uM[o], vMS);
-                vMA = fma(wa, uM[o], vMA);
-                vSM = fma(wm, uS[o], vSM);
-                vAM = fma(wm, uA[o], vAM);
-                vAA = fma(wa, uA[o], vAA);
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-              zM[i] = fma(op.c.mass[i][j], vMM, zM[i]);
-              zS[i] = fma(op.c.S[0][i][j], vMM, zS[i]);
-              zM[i] = fma(op.c.S[1][i][j], vSM, zM[i]);
-              zM[i] = fma(op.c.S[2][i][j], vMS, zM[i]);
-              zA[i] = fma(op.c.AA[0][i][j], vAM, zA[i]);
-              zA[i] = fma(op.c.AA[1][i][j], vMA, zA[i]);
-              zM[i] = fma(op.c.AA[2][i][j], vAA, zM[i]);
-            }
+          for (int o = 1; o <= P; ++o) {
+            const double lo = uM[-o], hi = uM[o];
+            const double sp = lo + hi, sm = hi - lo;
+            a1 = fma(op.tM[o], sp, a1);
+            a2 = fma(op.tS[o], sp, a2);
+            a3 = fma(op.tA[o], sm, a3);
           }
-          // ---- stage C: scatter along direction 0 into the ring
-#pragma unroll
-          for (int o = -P; o <= P; ++o) {
-            const int t = s + o;
-            if (t >= c0 && t < c1) {
-              const size_t wi = (size_t)t * R + P - o;
-              const double wM = __ldg(op.bM + wi), wS = __ldg(op.bS + wi), wA = __ldg(op.bA + wi);
-              const int slot = (ph + o + R) % R;
-#pragma unroll
-              for (int i = 0; i < NC; ++i) acc[i][slot] = fma(wM, zM[i], fma(wS, zS[i], fma(wA, zA[i], acc[i][slot])));
-            }
-          }
+          vMM = a1; vMS = a2; vMA = a3;
         }
         {
-          const int t = s - P;
-          const int slot = (ph + R - P) % R;
-          if (t >= c0 && t < c1 && active) {
-            const size_t pt = (size_t)t * ms + (size_t)gr * m + gc;
-            double Dv[NC];
+          double a1 = op.tM[0] * uS[0];
 #pragma unroll
-            for (int i = 0; i < NC; ++i) Dv[i] = 1.0;
-            if (mode >= EPI_JACOBI) {
-              const double M0 = __ldg(op.bM + (size_t)t * R + P), S0 = __ldg(op.bS + (size_t)t * R + P);
-              const double M1 = __ldg(op.bM + (size_t)gr * R + P), S1 = __ldg(op.bS + (size_t)gr * R + P);
-              const double M2 = __ldg(op.bM + (size_t)gc * R + P), S2 = __ldg(op.bS + (size_t)gc * R + P);
-#pragma unroll
-              for (int i = 0; i < NC; ++i)
-                Dv[i] = op.c.mass[i][i] * M0 * M1 * M2 + op.c.S[0][i][i] * S0 * M1 * M2 +
-                        op.c.S[1][i][i] * M0 * S1 * M2 + op.c.S[2][i][i] * M0 * M1 * S2;
-            }
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-              const double a = acc[i][slot];
-              const size_t gi = (size_t)i * m3 + pt;
-              double out;
-              if (mode == EPI_APPLY) out = a;
-              else if (mode == EPI_RESID) out = ep.b[gi] - a;
-              else if (mode == EPI_JACOBI) out = x[gi] + ep.omega * (ep.b[gi] - a) / Dv[i];
-              else out = a / Dv[i];
-              y[gi] = out;
-              if (dot == DOT_X_OUT) dsum = fma(x[gi], out, dsum);
-              else if (dot == DOT_OUT_OUT) dsum = fma(out, out, dsum);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < NC; ++i) acc[i][slot] = 0.0;
+          for (int o = 1; o <= P; ++o) a1 = fma(op.tM[o], uS[-o] + uS[o], a1);
+          vSM = a1;
         }
-        if (more) sstore(buf ^ 1);
-        __syncthreads();
+        {
+          const double c = uA[0];
+          double a1 = op.tM[0] * c, a3 = 0.0;
+#pragma unroll
+          for (int o = 1; o <= P; ++o) {
+            const double lo = uA[-o], hi = uA[o];
+            a1 = fma(op.tM[o], lo + hi, a1);
+            a3 = fma(op.tA[o], hi - lo, a3);
+          }
+          vAM = a1; vAA = a3;
+        }
+        if (zoneB) {
+          const double* rM = op.bM + (size_t)gc * R + P;
+          const double* rS = op.bS + (size_t)gc * R + P;
+          const double* rA = op.bA + (size_t)gc * R + P;
+          vMM = vMS = vMA = vSM = vAM = vAA = 0.0;
+#pragma unroll
+          for (int o = -P; o <= P; ++o) {
+            const double wm = __ldg(rM + o), ws = __ldg(rS + o), wa = __ldg(rA + o);
+            vMM = fma(wm, uM[o], vMM);
+            vMS = fma(ws, uM[o], vMS);
+            vMA = fma(wa, uM[o], vMA);
+            vSM = fma(wm, uS[o], vSM);
+            vAM = fma(wm, uA[o], vAM);
+            vAA = fma(wa, uA[o], vAA);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          zM[i] = fma(op.c.mass[i][j], vMM, zM[i]);
+          zS[i] = fma(op.c.S[0][i][j], vMM, zS[i]);
+          zM[i] = fma(op.c.S[1][i][j], vSM, zM[i]);
+          zM[i] = fma(op.c.S[2][i][j], vMS, zM[i]);
+          zA[i] = fma(op.c.AA[0][i][j], vAM, zA[i]);
+          zA[i] = fma(op.c.AA[1][i][j], vMA, zA[i]);
+          zM[i] = fma(op.c.AA[2][i][j], vAA, zM[i]);
+        }
+      }
+      // ---- stage C: scatter along direction 0 into the ring
+      const double* w = wts + buf * 3 * R;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double wM = w[r], wS = w[R + r], wA = w[2 * R + r];
+#pragma unroll
+        for (int i = 0; i < NC; ++i) acc[i][r] = fma(wM, zM[i], fma(wS, zS[i], fma(wA, zA[i], acc[i][r])));
       }
     }
+    {
+      const int t = s - P;
+      if (t >= c0 && t < c1 && active) {
+        const size_t pt = (size_t)t * ms + (size_t)gr * m + gc;
+        double Dv[NC];
+#pragma unroll
+        for (int i = 0; i < NC; ++i) Dv[i] = 1.0;
+        if (mode >= EPI_JACOBI) {
+          const double M0 = __ldg(op.bM + (size_t)t * R + P), S0 = __ldg(op.bS + (size_t)t * R + P);
+          const double M1 = __ldg(op.bM + (size_t)gr * R + P), S1 = __ldg(op.bS + (size_t)gr * R + P);
+          const double M2 = __ldg(op.bM + (size_t)gc * R + P), S2 = __ldg(op.bS + (size_t)gc * R + P);
+#pragma unroll
+          for (int i = 0; i < NC; ++i)
+            Dv[i] = op.c.mass[i][i] * M0 * M1 * M2 + op.c.S[0][i][i] * S0 * M1 * M2 +
+                    op.c.S[1][i][i] * M0 * S1 * M2 + op.c.S[2][i][i] * M0 * M1 * S2;
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          const double a = acc[i][0];
+          const size_t gi = (size_t)i * m3 + pt;
+          double out;
+          if (mode == EPI_APPLY) out = a;
+          else if (mode == EPI_RESID) out = ep.b[gi] - a;
+          else if (mode == EPI_JACOBI) out = x[gi] + ep.omega * (ep.b[gi] - a) / Dv[i];
+          else out = a / Dv[i];
+          y[gi] = out;
+          if (dot == DOT_X_OUT) dsum = fma(x[gi], out, dsum);
+          else if (dot == DOT_OUT_OUT) dsum = fma(out, out, dsum);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+#pragma unroll
+        for (int r = 0; r < R - 1; ++r) acc[i][r] = acc[i][r + 1];
+        acc[i][R - 1] = 0.0;
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
   }
   if (dot != DOT_NONE) {
 #pragma unroll
