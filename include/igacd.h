@@ -67,6 +67,7 @@ int igacd_get_info(igacd_handle h, int* dim, int* p, int* levels);
 int igacd_num_levels(igacd_handle h, int* levels);
 int igacd_level_n(igacd_handle h, int level, int* n);
 int igacd_ndof(igacd_handle h, int level, size_t* ndof);
+/* omega and rho of the active smoother on `level` (Jacobi: rho(D^-1 A); Toeplitz: rho(T^-1 A)). */
 int igacd_smoother_omega(igacd_handle h, int level, double* omega, double* rho);
 
 /* y = A_level x   (R2).  x, y device, length igacd_ndof(h, level); x != y. */
@@ -75,8 +76,9 @@ int igacd_apply(igacd_handle h, int level, const double* x, double* y, void* str
 /* r = b - A_level x   (R2 with the residual epilogue). */
 int igacd_residual(igacd_handle h, int level, const double* b, const double* x, double* r, void* stream);
 
-/* `sweeps` damped-Jacobi sweeps x <- x + omega_l D_l^{-1} (b - A_l x) in place on x (R4).
- * omega_l as reported by igacd_smoother_omega unless omega > 0 is given (then used as is). */
+/* `sweeps` damped-Jacobi sweeps x <- x + omega_l D_l^{-1} (b - A_l x) in place on x (R4),
+ * whatever smoother the V-cycle uses.  omega_l = the Jacobi parameter of the level unless
+ * omega > 0 is given (then used as is). */
 int igacd_smooth(igacd_handle h, int level, const double* b, double* x, int sweeps, double omega, void* stream);
 
 /* x_coarse = P_level^T x_fine   (R3, restriction to level+1). */
@@ -98,6 +100,19 @@ int igacd_vcycle(igacd_handle h, const double* b, double* x, void* stream);
 int igacd_precond(igacd_handle h, const double* b, double* x, void* stream);
 int igacd_set_preconditioner(igacd_handle h, int mode);
 int igacd_get_preconditioner(igacd_handle h, int* mode);
+
+/* V-cycle smoother (both systems, all levels but the coarsest):
+ *   IGACD_SMOOTH_JACOBI   (reading R4)  x <- x + omega_l D_l^{-1} (b - A_l x)
+ *   IGACD_SMOOTH_TOEPLITZ (reading R4', default) x <- x + omega_t,l T^{-1} (b - A_l x) with the
+ *     paper's T_n^p = I_d (x) T(m_{p-1}) (x) .. (x) T(m_{p-1}), applied by
+ *     batched banded line solves.  omega from power iteration on D^{-1}A resp. T^{-1}A.
+ * igacd_aux_is_exact: 1 when the auxiliary operator is one Kronecker product (b0 along a
+ * coordinate axis) and is inverted exactly by line solves instead of a V-cycle. */
+#define IGACD_SMOOTH_JACOBI 0
+#define IGACD_SMOOTH_TOEPLITZ 1
+int igacd_set_smoother(igacd_handle h, int kind);
+int igacd_get_smoother(igacd_handle h, int* kind);
+int igacd_aux_is_exact(igacd_handle h, int* exact);
 
 /* Auxiliary scalar operator: s_out = A_s s_in on `level` (vectors of igacd_ndof/dim doubles),
  * and its smoother parameters.  IGACD_E_ARG when the handle has no auxiliary space. */

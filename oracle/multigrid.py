@@ -11,6 +11,10 @@ Readings (DESIGN.md):
       omega_l = 4/(3 * 1.05 * rho_l), rho_l = generalized Rayleigh quotient
       (v,A v)/(v,D v) after K=30 normalised power steps v <- D^{-1}A v / ||.||_2 from the
       counter-based start vector inputs.hash_vector (same formula on both sides).
+  R4' smoother = Richardson with the paper's preconditioner T_n^p = I_d (x) T(m_{p-1})^{(x)d}
+      (T entries phi_{2p-1}(p - i + j), |i-j| < p):
+      x <- x + omega_t T^{-1}(b - A x), omega_t = 4/(3 * 1.05 * rho_t), rho_t = ||T^{-1} A v||
+      after K=30 normalised steps v <- T^{-1} A v / ||.||_2 from the same start vector.
   R5  coarsest level solved exactly (dense Cholesky, library primitive scipy cho_solve).
   R6  levels: n_{l+1} = n_l/2 while n_l is even, the next interior size n_l/2+p-2 >= 1 and
       d*(n_l+p-2)^d > 1500 (or exactly ``levels`` levels when requested).
@@ -25,8 +29,10 @@ Readings (DESIGN.md):
 import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
+import scipy.sparse.linalg as spl
 
 from inputs import hash_vector
+from .bspline import cardinal
 from .transfer import prolongation
 
 NCOARSE_MAX = 1500
@@ -56,10 +62,29 @@ def power_rho(A: sp.spmatrix, Ddiag: np.ndarray, steps: int = POWER_STEPS) -> fl
     return float(v @ (A @ v)) / float(v @ (Ddiag * v))
 
 
+def toeplitz_T(p: int, m: int) -> np.ndarray:
+    """T_m(m_{p-1}) of PAPER.md:1204-1210: (i,j) -> phi_{2p-1}(p - i + j) if |i-j| < p."""
+    T = np.zeros((m, m))
+    for i in range(m):
+        for j in range(max(0, i - p + 1), min(m, i + p)):
+            T[i, j] = cardinal(2 * p - 1, p - i + j)
+    return T
+
+
+def power_rho_t(A: sp.spmatrix, Tsolve, steps: int = POWER_STEPS) -> float:
+    """rho_t = ||T^{-1} A v|| after ``steps`` normalised steps of v <- T^{-1} A v (reading R4')."""
+    v = hash_vector(A.shape[0])
+    for _ in range(steps):
+        w = Tsolve(A @ v)
+        v = w / np.linalg.norm(w)
+    return float(np.linalg.norm(Tsolve(A @ v)))
+
+
 class Hierarchy:
     def __init__(self, A0: sp.spmatrix, d: int, p: int, n: int, levels: int = 0, nu_pre: int = 1, nu_post: int = 1,
-                 ncomp: int = None, ns=None):
+                 ncomp: int = None, ns=None, smoother: str = "toeplitz"):
         self.d, self.p = d, p
+        self.smoother = smoother
         self.ns = level_sizes(d, p, n, levels) if ns is None else list(ns)
         self.A = [sp.csr_matrix(A0)]
         self.P = []
@@ -70,6 +95,17 @@ class Hierarchy:
         self.D = [A.diagonal().copy() for A in self.A]
         self.rho = [power_rho(self.A[l], self.D[l]) for l in range(len(self.A) - 1)]
         self.omega = [4.0 / (3.0 * 1.05 * r) for r in self.rho]
+        nc = d if ncomp is None else ncomp
+        self.Tlu, self.rho_t, self.omega_t = [], [], []
+        for l in range(len(self.A) - 1):
+            T1 = sp.csr_matrix(toeplitz_T(p, self.ns[l] + p - 2))
+            K = T1
+            for _ in range(d - 1):
+                K = sp.kron(K, T1, format="csr")
+            lu = spl.splu(sp.kron(sp.identity(nc, format="csr"), K, format="csc"))
+            self.Tlu.append(lu)
+            self.rho_t.append(power_rho_t(self.A[l], lu.solve))
+            self.omega_t.append(4.0 / (3.0 * 1.05 * self.rho_t[-1]))
         self.nu_pre, self.nu_post = nu_pre, nu_post
         self.coarse = sla.cho_factor(self.A[-1].toarray(), lower=True)
 
@@ -83,16 +119,25 @@ class Hierarchy:
             x = x + self.omega[l] * (b - self.A[l] @ x) / self.D[l]
         return x
 
+    def toeplitz(self, l, b, x, sweeps):
+        """sweeps x <- x + omega_t,l T^{-1} (b - A_l x)   (reading R4')."""
+        for _ in range(sweeps):
+            x = x + self.omega_t[l] * self.Tlu[l].solve(b - self.A[l] @ x)
+        return x
+
+    def smooth(self, l, b, x, sweeps):
+        return (self.toeplitz if self.smoother == "toeplitz" else self.jacobi)(l, b, x, sweeps)
+
     def vcycle(self, b, l: int = 0):
         """One V-cycle for A_l e = b from a zero initial guess (steps 1-3)."""
         if l == self.L:
             return sla.cho_solve(self.coarse, b)
         x = np.zeros_like(b)
-        x = self.jacobi(l, b, x, self.nu_pre)                     # step 1: pre-smoothing
+        x = self.smooth(l, b, x, self.nu_pre)                     # step 1: pre-smoothing
         r = b - self.A[l] @ x                                     # step 2: residual,
         e = self.vcycle(self.P[l].T @ r, l + 1)                   #   restrict, recurse,
         x = x + self.P[l] @ e                                     #   prolongate and correct
-        x = self.jacobi(l, b, x, self.nu_post)                    # step 3: post-smoothing
+        x = self.smooth(l, b, x, self.nu_post)                    # step 3: post-smoothing
         return x
 
 
@@ -102,17 +147,26 @@ def aux_map(d: int, nscal: int, b0) -> sp.csr_matrix:
 
 
 class AuxPreconditioner:
-    """Reading R8: z = Pi Vs Pi^T r;  z += V (r - A z);  z += Pi Vs Pi^T (r - A z)."""
+    """Reading R8: z = Pi Bs Pi^T r;  z += V (r - A z);  z += Pi Bs Pi^T (r - A z).
 
-    def __init__(self, A0, d, p, n, b0, levels=0, nu_pre=1, nu_post=1):
+    Bs = exact A_s^{-1} (sparse LU, library primitive) when b0 has exactly one nonzero
+    component (A_s is then one Kronecker product), else the V-cycle of A_s."""
+
+    def __init__(self, A0, d, p, n, b0, levels=0, nu_pre=1, nu_post=1, smoother="toeplitz"):
         self.A = sp.csr_matrix(A0)
-        self.V = Hierarchy(A0, d, p, n, levels, nu_pre, nu_post)
+        self.V = Hierarchy(A0, d, p, n, levels, nu_pre, nu_post, smoother=smoother)
         self.Pi = aux_map(d, A0.shape[0] // d, b0)
         As = sp.csr_matrix(self.Pi.T @ self.A @ self.Pi)                # A_s := Pi^T A Pi
-        self.Vs = Hierarchy(As, d, p, n, levels, nu_pre, nu_post, ncomp=1, ns=self.V.ns)
+        self.exact = sum(1 for v in b0 if v != 0.0) == 1
+        if self.exact:
+            self.lu = spl.splu(As.tocsc())
+            self.Bs = self.lu.solve
+        else:
+            self.Vs = Hierarchy(As, d, p, n, levels, nu_pre, nu_post, ncomp=1, ns=self.V.ns, smoother=smoother)
+            self.Bs = self.Vs.vcycle
 
     def __call__(self, r):
-        z = self.Pi @ self.Vs.vcycle(self.Pi.T @ r)
+        z = self.Pi @ self.Bs(self.Pi.T @ r)
         z = z + self.V.vcycle(r - self.A @ z)
-        z = z + self.Pi @ self.Vs.vcycle(self.Pi.T @ (r - self.A @ z))
+        z = z + self.Pi @ self.Bs(self.Pi.T @ (r - self.A @ z))
         return z

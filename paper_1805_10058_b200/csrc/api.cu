@@ -72,7 +72,25 @@ static std::vector<int> level_sizes(int d, int p, int n, int levels) {
   return ns;
 }
 
+// Cardinal B-spline phi_p(t), host side, for the entries of
+// T_m(m_{p-1}): (i,j) -> phi_{2p-1}(p - i + j) for |i-j| < p.
+static double cardinal_host(int p, double t) {
+  if (p == 0) return (t >= 0.0 && t < 1.0) ? 1.0 : 0.0;
+  return t / p * cardinal_host(p - 1, t) + (p + 1 - t) / p * cardinal_host(p - 1, t - 1.0);
+}
+
+static void build_toeplitz_factor(int p, Level& L) {
+  const int m = L.m, w = p - 1;
+  std::vector<double> F((size_t)m * (2 * w + 1), 0.0), Lb, inv;
+  for (int i = 0; i < m; ++i)
+    for (int o = -w; o <= w; ++o)
+      if (i + o >= 0 && i + o < m) F[(size_t)i * (2 * w + 1) + o + w] = cardinal_host(2 * p - 1, p + o);
+  band_cholesky(F, m, w, Lb, inv);
+  L.T.upload(Lb, inv, m, w);
+}
+
 static void free_system(System& S) {
+  for (int a = 0; a < 3; ++a) S.tf[a].release();
   for (auto& L : S.lv) {
     cudaFree(L.b);
     cudaFree(L.x);
@@ -86,8 +104,10 @@ static void free_system(System& S) {
 
 static void destroy_handle(Handle* h) {
   if (!h) return;
-  for (auto& L : h->lv)
+  for (auto& L : h->lv) {
     for (int f = 0; f < 3; ++f) cudaFree(L.band[f]);
+    L.T.release();
+  }
   for (auto& T : h->tr) {
     cudaFree(T.p_start);
     cudaFree(T.p_w);
@@ -141,6 +161,37 @@ static void estimate_omega(Handle& h, int sy, int l, cudaStream_t s) {
   L.omega = 4.0 / (3.0 * 1.05 * L.rho);
 }
 
+// z <- T^{-1} z (in place) for system sy at level l: one band solve per direction
+static void apply_tinv(Handle& h, int sy, int l, double* z, cudaStream_t s) {
+  for (int a = 0; a < h.dim; ++a) launch_band_solve(h, h.sys[sy].nc, l, a, h.lv[l].T, z, 0, 0.0, nullptr, s);
+}
+
+// Reading R4': rho_t = ||T^{-1} A v|| after POWER_STEPS normalised steps v <- T^{-1} A v / ||.||
+// from the counter-based start vector; omega_t = 4 / (3 * 1.05 * rho_t).
+static void estimate_omega_t(Handle& h, int sy, int l, cudaStream_t s) {
+  SysLevel& L = h.sys[sy].lv[l];
+  double* v = L.x;
+  double* w = L.t;
+  launch_hash_vector(h, v, L.ndof, s);
+  Epi ep{};
+  const int nv = vec_ctas(L.ndof);
+  double nrm = 0.0;
+  for (int it = 0; it <= POWER_STEPS; ++it) {
+    launch_operator(h, sy, l, v, w, EPI_APPLY, DOT_NONE, ep, s);
+    apply_tinv(h, sy, l, w, s);
+    launch_dot(h, w, w, L.ndof, h.partial, s);
+    if (it == POWER_STEPS) {
+      nrm = std::sqrt(reduce_to_host(h, nv, S_A, s));
+      break;
+    }
+    launch_finalize(h, h.partial, nv, h.scal + S_NORM, s);
+    launch_scale(h, w, h.scal + S_NORM, nullptr, L.ndof, s);
+    std::swap(v, w);
+  }
+  L.rho_t = nrm;
+  L.omega_t = 4.0 / (3.0 * 1.05 * L.rho_t);
+}
+
 static void setup_system(Handle& h, int sy, int nc, const Coef& coef, cudaStream_t s) {
   System& S = h.sys[sy];
   S.nc = nc;
@@ -159,7 +210,36 @@ static void setup_system(Handle& h, int sy, int nc, const Coef& coef, cudaStream
   // the dense coarse inverse is built only when the coarsest level is small enough;
   // otherwise the system still applies its operator but refuses V-cycles
   if (S.lv.back().ndof <= COARSE_DENSE_MAX) build_coarse_inverse(h, sy, s);
-  for (size_t l = 0; l + 1 < h.lv.size(); ++l) estimate_omega(h, sy, (int)l, s);
+  for (size_t l = 0; l + 1 < h.lv.size(); ++l) {
+    estimate_omega(h, sy, (int)l, s);
+    estimate_omega_t(h, sy, (int)l, s);
+  }
+}
+
+// Reading R8: when A_s is a single Kronecker product (b0 along a coordinate axis l):
+// A_s = (c_m M + c_s S)_l (x) M (x) ..; factor each 1D matrix once (level 0).
+static void setup_aux_tensor(Handle& h, cudaStream_t s) {
+  System& A = h.sys[1];
+  const Coef& c = A.coef;
+  int nS = 0, lS = -1;
+  for (int l = 0; l < h.dim; ++l)
+    if (c.S[l][0][0] != 0.0) { ++nS; lS = l; }
+  bool aa = false;
+  for (int q = 0; q < 3; ++q) aa = aa || c.AA[q][0][0] != 0.0;
+  if (aa || nS > 1) return;
+  const Level& L0 = h.lv[0];
+  const int m = L0.m, p = h.p, W = 2 * p + 1;
+  const int lead = lS >= 0 ? lS : 0;   // the direction that carries the scalar coefficients
+  for (int a = 0; a < h.dim; ++a) {
+    std::vector<double> F((size_t)m * W), Lb, inv;
+    for (size_t k = 0; k < F.size(); ++k) {
+      if (a != lead) F[k] = L0.hband[0][k];                                       // M
+      else F[k] = c.mass[0][0] * L0.hband[0][k] + (lS >= 0 ? c.S[lS][0][0] * L0.hband[2][k] : 0.0);
+    }
+    band_cholesky(F, m, p, Lb, inv);
+    A.tf[a].upload(Lb, inv, m, p);
+  }
+  A.tensor_exact = true;
 }
 
 // Reading R8: patterns of A_s = Pi^T A Pi, Pi s = b0 s:  C_s = sum_ij b0_i C[i][j] b0_j.
@@ -205,6 +285,7 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
       L.nscal = 1;
       for (int a = 0; a < dim; ++a) L.nscal *= (size_t)L.m;
       assemble_level(*h, L, s);
+      build_toeplitz_factor(p, L);
     }
     h->tr.resize(ns.size() - 1);
     size_t scratch = 1;
@@ -231,7 +312,10 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
     // auxiliary space span{b0 s} (reading R8) when the b0-term is present
     const Coef ac = aux_patterns(dim, coef, h->b0);
     h->has_aux = bb > 0.0 && ac.mass[0][0] + ac.S[0][0][0] + ac.S[1][0][0] + ac.S[2][0][0] > 0.0;
-    if (h->has_aux) setup_system(*h, 1, 1, ac, s);
+    if (h->has_aux) {
+      setup_system(*h, 1, 1, ac, s);
+      setup_aux_tensor(*h, s);
+    }
     h->precond = h->has_aux ? PRECOND_AUX : PRECOND_VCYCLE;
     IGACD_CUDA(cudaStreamSynchronize(s));
   } catch (...) {
@@ -253,6 +337,39 @@ static void jacobi_sweeps(Handle& h, int sy, int l, const double* b, double*& cu
   }
 }
 
+// `sweeps` smoothing steps on x for A_l x = b (system sy).  from_zero: x is 0 on entry, so the
+// first step needs no operator apply.  JACOBI (R4): x <- x + omega D^{-1}(b - A x), ping-pong
+// buffers; TOEPLITZ (R4'): x <- x + omega_t T^{-1}(b - A x), T = T_n^p, in place.
+static void smooth(Handle& h, int sy, int l, const double* b, double*& cur, double*& oth, int sweeps, bool from_zero,
+                   cudaStream_t s) {
+  SysLevel& L = h.sys[sy].lv[l];
+  if (sweeps <= 0) {
+    if (from_zero) launch_zero(h, cur, L.ndof, s);
+    return;
+  }
+  if (h.smoother == SMOOTH_JACOBI) {
+    int k = 0;
+    if (from_zero) {
+      launch_scale_dinv(h, sy, l, b, cur, L.omega, s);   // first sweep from x = 0: x = omega D^-1 b
+      k = 1;
+    }
+    jacobi_sweeps(h, sy, l, b, cur, oth, sweeps - k, L.omega, s);
+    return;
+  }
+  Epi ep{};
+  ep.b = b;
+  for (int k = 0; k < sweeps; ++k) {
+    if (k == 0 && from_zero) {
+      launch_copy(h, b, L.r, L.ndof, s);
+      launch_zero(h, cur, L.ndof, s);
+    } else {
+      launch_operator(h, sy, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
+    }
+    for (int a = 0; a + 1 < h.dim; ++a) launch_band_solve(h, h.sys[sy].nc, l, a, h.lv[l].T, L.r, 0, 0.0, nullptr, s);
+    launch_band_solve(h, h.sys[sy].nc, l, h.dim - 1, h.lv[l].T, L.r, 1, L.omega_t, cur, s);
+  }
+}
+
 // x = V_l b from a zero initial guess (pre-smooth, residual,
 // restrict, recurse, prolongate-and-correct, post-smooth).  The result lands in x.
 static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, cudaStream_t s) {
@@ -266,15 +383,10 @@ static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, c
     return;
   }
   SysLevel& L = S.lv[l];
-  const int swaps = std::max(0, h.nu_pre - 1) + h.nu_post;
+  const int swaps = h.smoother == SMOOTH_JACOBI ? std::max(0, h.nu_pre - 1) + h.nu_post : 0;
   double* cur = (swaps % 2 == 0) ? x : L.t;
   double* oth = (cur == x) ? L.t : x;
-  if (h.nu_pre >= 1) {
-    launch_scale_dinv(h, sy, l, b, cur, L.omega, s);   // first sweep from x = 0: x = omega D^-1 b
-    jacobi_sweeps(h, sy, l, b, cur, oth, h.nu_pre - 1, L.omega, s);
-  } else {
-    launch_zero(h, cur, L.ndof, s);
-  }
+  smooth(h, sy, l, b, cur, oth, h.nu_pre, true, s);
   Epi ep{};
   ep.b = b;
   launch_operator(h, sy, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
@@ -282,8 +394,19 @@ static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, c
   launch_restrict(h, S.nc, l, L.r, C.b, s);
   vcycle_level(h, sy, l + 1, C.b, C.x, s);
   launch_prolong(h, S.nc, l, C.x, cur, true, s);
-  jacobi_sweeps(h, sy, l, b, cur, oth, h.nu_post, L.omega, s);
+  smooth(h, sy, l, b, cur, oth, h.nu_post, false, s);
   if (cur != x) launch_copy(h, cur, x, L.ndof, s);
+}
+
+// approximate (V-cycle) or exact (tensor, reading R8) solve of the auxiliary system at level 0
+static void aux_solve(Handle& h, const double* sb, double* sx, cudaStream_t s) {
+  System& A = h.sys[1];
+  if (A.tensor_exact) {
+    launch_copy(h, sb, sx, A.lv[0].ndof, s);
+    for (int a = 0; a < h.dim; ++a) launch_band_solve(h, 1, 0, a, A.tf[a], sx, 0, 0.0, nullptr, s);
+    return;
+  }
+  vcycle_level(h, 1, 0, sb, sx, s);
 }
 
 // Preconditioner action z = B r (reading R8).  PRECOND_VCYCLE: B = V.  PRECOND_AUX: the
@@ -300,14 +423,14 @@ static void precond_apply(Handle& h, const double* r, double* z, cudaStream_t s)
   Epi ep{};
   ep.b = r;
   launch_pi_t(h, r, a0.b, s);
-  vcycle_level(h, 1, 0, a0.b, a0.x, s);
+  aux_solve(h, a0.b, a0.x, s);
   launch_pi(h, a0.x, z, false, s);
   launch_operator(h, 0, 0, z, h.ar, EPI_RESID, DOT_NONE, ep, s);
   vcycle_level(h, 0, 0, h.ar, h.aw, s);
   launch_axpy_inplace(h, h.aw, z, h.lv.empty() ? 0 : h.sys[0].lv[0].ndof, s);
   launch_operator(h, 0, 0, z, h.ar, EPI_RESID, DOT_NONE, ep, s);
   launch_pi_t(h, h.ar, a0.b, s);
-  vcycle_level(h, 1, 0, a0.b, a0.x, s);
+  aux_solve(h, a0.b, a0.x, s);
   launch_pi(h, a0.x, z, true, s);
 }
 
@@ -477,8 +600,11 @@ int igacd_ndof(igacd_handle h, int level, size_t* ndof) {
 int igacd_smoother_omega(igacd_handle h, int level, double* omega, double* rho) {
   API_BEGIN
   check_level(H(h), level);
-  if (omega) *omega = H(h)->sys[0].lv[level].omega;
-  if (rho) *rho = H(h)->sys[0].lv[level].rho;
+  Handle* hh = H(h);
+  const SysLevel& L = hh->sys[0].lv[level];
+  const bool t = hh->smoother == SMOOTH_TOEPLITZ;
+  if (omega) *omega = t ? L.omega_t : L.omega;
+  if (rho) *rho = t ? L.rho_t : L.rho;
   API_END
 }
 
@@ -574,6 +700,28 @@ int igacd_set_preconditioner(igacd_handle h, int mode) {
   API_END
 }
 
+int igacd_set_smoother(igacd_handle h, int kind) {
+  API_BEGIN
+  if (kind != SMOOTH_JACOBI && kind != SMOOTH_TOEPLITZ) throw Error{IGACD_E_ARG, "unknown smoother"};
+  H(h)->smoother = kind;
+  API_END
+}
+
+int igacd_get_smoother(igacd_handle h, int* kind) {
+  API_BEGIN
+  check_ptr(kind);
+  *kind = H(h)->smoother;
+  API_END
+}
+
+int igacd_aux_is_exact(igacd_handle h, int* exact) {
+  API_BEGIN
+  check_ptr(exact);
+  Handle* hh = H(h);
+  *exact = hh->has_aux && hh->sys[1].tensor_exact ? 1 : 0;
+  API_END
+}
+
 int igacd_get_preconditioner(igacd_handle h, int* mode) {
   API_BEGIN
   check_ptr(mode);
@@ -598,8 +746,10 @@ int igacd_aux_omega(igacd_handle h, int level, double* omega, double* rho) {
   Handle* hh = H(h);
   check_level(hh, level);
   if (!hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space on this handle"};
-  if (omega) *omega = hh->sys[1].lv[level].omega;
-  if (rho) *rho = hh->sys[1].lv[level].rho;
+  const SysLevel& L = hh->sys[1].lv[level];
+  const bool t = hh->smoother == SMOOTH_TOEPLITZ;
+  if (omega) *omega = t ? L.omega_t : L.omega;
+  if (rho) *rho = t ? L.rho_t : L.rho;
   API_END
 }
 

@@ -58,6 +58,15 @@ struct Transfer1D {   // 1D prolongation P (m_f x m_c) in fixed-width row storag
   std::vector<double> hdense;   // host dense copy (debug/parity)
 };
 
+// Banded Cholesky factor F = L L^T on the device (linesolve.cu).
+struct BandFactor {
+  int m = 0, w = 0;
+  double* Lb = nullptr;    // [m][w+1]: L[k][k-j] at k*(w+1) + (w-j)
+  double* inv = nullptr;   // [m]: 1/L[k][k]
+  void upload(const std::vector<double>& Lb_h, const std::vector<double>& inv_h, int m_, int w_);
+  void release();
+};
+
 // Geometry of one level (shared by the vector system and the auxiliary scalar system).
 struct Level {
   int n = 0, m = 0;
@@ -65,13 +74,17 @@ struct Level {
   double* band[3] = {nullptr, nullptr, nullptr};  // M, A, S
   std::vector<double> hband[3];
   OpParams geo;  // m, zones, bands, Toeplitz rows (coefficients filled per system)
+  BandFactor T;  // Cholesky factor of T_{m}(m_{p-1}), the smoother's 1D factor
 };
+
+enum Smoother { SMOOTH_JACOBI = 0, SMOOTH_TOEPLITZ = 1 };
 
 // Per-level state of one system.
 struct SysLevel {
   OpParams op;         // geometry of the level + this system's pattern coefficients
   size_t ndof = 0;
-  double rho = 0.0, omega = 0.0;
+  double rho = 0.0, omega = 0.0;     // damped Jacobi (reading R4)
+  double rho_t = 0.0, omega_t = 0.0; // Toeplitz-preconditioned Richardson (reading R4')
   double* b = nullptr;  // work vectors (ndof each)
   double* x = nullptr;
   double* t = nullptr;
@@ -85,6 +98,10 @@ struct System {
   Coef coef;
   std::vector<SysLevel> lv;
   double* cinv = nullptr;   // dense inverse of the coarsest level
+  // exact tensor inverse of the level-0 operator when it is a single Kronecker product
+  // (auxiliary system with b0 along a coordinate axis): one factor per direction
+  bool tensor_exact = false;
+  BandFactor tf[3];
 };
 
 enum Precond { PRECOND_VCYCLE = 0, PRECOND_AUX = 1 };
@@ -98,6 +115,7 @@ struct Handle {
   System sys[2];                // 0: vector operator, 1: auxiliary scalar operator
   bool has_aux = false;
   int precond = PRECOND_VCYCLE;
+  int smoother = SMOOTH_TOEPLITZ;
   // transfer scratch (max size), reductions
   double* scratch0 = nullptr;
   double* scratch1 = nullptr;
@@ -172,6 +190,11 @@ void launch_pcg_update_xr(Handle& h, double* x, double* r, const double* p, cons
                           const double* rz, const double* pq, double* partial, cudaStream_t s);
 void launch_pcg_update_p(Handle& h, double* p, const double* z, size_t n, const double* rz_new,
                          const double* rz_old, cudaStream_t s);
+
+// ---- linesolve.cu -------------------------------------------------------------------
+void band_cholesky(const std::vector<double>& F, int m, int w, std::vector<double>& Lb, std::vector<double>& inv);
+void launch_band_solve(Handle& h, int nc, int level, int axis, const BandFactor& F, double* data, int mode,
+                       double omega, double* xacc, cudaStream_t s);
 
 // ---- common -------------------------------------------------------------------------
 inline void count_launch(Handle& h) { h.launches++; }

@@ -48,6 +48,9 @@ _vcycle = _sig("igacd_vcycle", [_vp, _vp, _vp, _vp])
 _precond = _sig("igacd_precond", [_vp, _vp, _vp, _vp])
 _set_precond = _sig("igacd_set_preconditioner", [_vp, _c_int])
 _get_precond = _sig("igacd_get_preconditioner", [_vp, _P(_c_int)])
+_set_smoother = _sig("igacd_set_smoother", [_vp, _c_int])
+_get_smoother = _sig("igacd_get_smoother", [_vp, _P(_c_int)])
+_aux_exact = _sig("igacd_aux_is_exact", [_vp, _P(_c_int)])
 _apply_aux = _sig("igacd_apply_aux", [_vp, _c_int, _vp, _vp, _vp])
 _aux_omega = _sig("igacd_aux_omega", [_vp, _c_int, _P(_c_double), _P(_c_double)])
 _solve = _sig("igacd_solve", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
@@ -61,6 +64,8 @@ _reset_prof = _sig("igacd_reset_profile", [_vp])
 IGACD_E_NOCONV = -4
 IGACD_PRECOND_VCYCLE = 0
 IGACD_PRECOND_AUX = 1
+IGACD_SMOOTH_JACOBI = 0
+IGACD_SMOOTH_TOEPLITZ = 1
 
 
 class IgacdError(RuntimeError):
@@ -182,6 +187,22 @@ def igacd_set_preconditioner(h, mode):
 def igacd_get_preconditioner(h):
     v = _c_int()
     _check(_get_precond(h, ctypes.byref(v)))
+    return v.value
+
+
+def igacd_set_smoother(h, kind):
+    _check(_set_smoother(h, kind))
+
+
+def igacd_get_smoother(h):
+    v = _c_int()
+    _check(_get_smoother(h, ctypes.byref(v)))
+    return v.value
+
+
+def igacd_aux_is_exact(h):
+    v = _c_int()
+    _check(_aux_exact(h, ctypes.byref(v)))
     return v.value
 
 

@@ -204,17 +204,20 @@ VCYCLE_CASES = [Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels
                 Case(3, 2, 8, nu=1.0, beta=0.1, levels=2), Case(3, 3, 8, nu=1.0, levels=2)]
 
 
+@pytest.mark.parametrize("smoother", ["toeplitz", "jacobi"])
 @pytest.mark.parametrize("case", VCYCLE_CASES, ids=repr)
-def test_vcycle_matches_oracle(case):
+def test_vcycle_matches_oracle(case, smoother):
     h = case.handle()
     try:
+        ig.igacd_set_smoother(h, ig.IGACD_SMOOTH_TOEPLITZ if smoother == "toeplitz" else ig.IGACD_SMOOTH_JACOBI)
         disc = Discretization(case.d, case.p, case.n)
         A = disc.assemble(case.form)
-        H = Hierarchy(A, case.d, case.p, case.n, case.levels)
+        H = Hierarchy(A, case.d, case.p, case.n, case.levels, smoother=smoother)
         assert ig.igacd_num_levels(h) == len(H.ns)
         for l in range(len(H.ns) - 1):
             w, rho = ig.igacd_smoother_omega(h, l)
-            assert abs(rho - H.rho[l]) <= 1e-10 * H.rho[l], (l, rho, H.rho[l])
+            ref = H.rho_t[l] if smoother == "toeplitz" else H.rho[l]
+            assert abs(rho - ref) <= 1e-10 * ref, (l, rho, ref)
         b = np.random.default_rng(11).uniform(-1, 1, disc.ndof)
         x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
         ig.igacd_vcycle(h, to_dev(b), x)
@@ -240,7 +243,8 @@ def test_aux_operator_matches_oracle(case):
         ig.igacd_destroy(h)
 
 
-@pytest.mark.parametrize("case", VCYCLE_CASES[:4], ids=repr)
+@pytest.mark.parametrize("case", VCYCLE_CASES[:4] + [Case(3, 3, 8, nu=1e-2, beta=1e-3, b0=(0.0, 0.0, 1.0), levels=2)],
+                         ids=repr)
 def test_aux_preconditioner_matches_oracle(case):
     h = case.handle()
     try:
@@ -248,9 +252,11 @@ def test_aux_preconditioner_matches_oracle(case):
         A = disc.assemble(case.form)
         B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels)
         assert ig.igacd_get_preconditioner(h) == ig.IGACD_PRECOND_AUX
-        for l in range(len(B.Vs.ns) - 1):
-            w, rho = ig.igacd_aux_omega(h, l)
-            assert abs(rho - B.Vs.rho[l]) <= 1e-10 * B.Vs.rho[l]
+        assert ig.igacd_aux_is_exact(h) == int(B.exact)
+        if not B.exact:
+            for l in range(len(B.Vs.ns) - 1):
+                w, rho = ig.igacd_aux_omega(h, l)
+                assert abs(rho - B.Vs.rho_t[l]) <= 1e-10 * B.Vs.rho_t[l]
         b = np.random.default_rng(13).uniform(-1, 1, disc.ndof)
         x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
         ig.igacd_precond(h, to_dev(b), x)
@@ -261,7 +267,8 @@ def test_aux_preconditioner_matches_oracle(case):
 
 SOLVE_CASES = [Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels=2),
                Case(2, 3, 32, nu=1.0, beta=0.1, levels=0), Case(3, 2, 8, nu=1.0, beta=0.1, levels=2),
-               Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2))]
+               Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)), Case(2, 5, 32, nu=1e-4, beta=1e-4, b0=(1.0, 0.0)),
+               Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0))]
 
 
 @pytest.mark.parametrize("case", SOLVE_CASES, ids=repr)
@@ -289,9 +296,10 @@ def test_plain_vcycle_preconditioner_solve():
     h = case.handle()
     try:
         ig.igacd_set_preconditioner(h, ig.IGACD_PRECOND_VCYCLE)
+        ig.igacd_set_smoother(h, ig.IGACD_SMOOTH_JACOBI)
         disc = Discretization(case.d, case.p, case.n)
         A = disc.assemble(case.form)
-        H = Hierarchy(A, case.d, case.p, case.n, case.levels)
+        H = Hierarchy(A, case.d, case.p, case.n, case.levels, smoother="jacobi")
         b = np.random.default_rng(5).uniform(-1, 1, disc.ndof)
         xo, ito, hist = pcg(A, b, H.vcycle, 1e-8, 2000)
         x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")

@@ -10,7 +10,7 @@ import scipy.sparse.linalg as spl
 import inputs
 from oracle import bspline as bs
 from oracle.krylov import pcg
-from oracle.multigrid import Hierarchy, level_sizes, power_rho
+from oracle.multigrid import AuxPreconditioner, Hierarchy, level_sizes, power_rho, power_rho_t, toeplitz_T
 from oracle.operator import Discretization, form_alfven
 from oracle.transfer import prolongation, prolongation_1d
 
@@ -112,11 +112,41 @@ def test_pcg_matches_direct_solve_and_counts():
     assert it0 == 0
 
 
-def test_config0_solves():
+@pytest.mark.parametrize("smoother", ["jacobi", "toeplitz"])
+def test_config0_solves(smoother):
     c = inputs.config(0)
     A = Discretization(c.dim, c.p, c.n).assemble(form_alfven(c.nu, c.beta, c.lam, c.b0))
-    H = Hierarchy(A, c.dim, c.p, c.n, c.levels)
+    B = AuxPreconditioner(A, c.dim, c.p, c.n, c.b0, c.levels, smoother=smoother)
+    assert B.exact          # b0 = (1, 0): exact auxiliary solve
     b = inputs.rhs(c)
-    x, it, hist = pcg(A, b, H.vcycle, c.tol, 1000)
+    x, it, hist = pcg(A, b, B, c.tol, 1000)
     assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) < 2 * c.tol
-    assert it < 100
+    assert it < 40
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_toeplitz_factor_entries_and_symbol(p):
+    # T_m(m_{p-1}) entries are cardinal B-spline values; it is the Toeplitz
+    # matrix of the symbol m_{p-1} (g_p): T = I for p = 1, eigenvalues in
+    # [min m_{p-1}, max m_{p-1}] = [m_{p-1}(pi), 1]
+    from oracle.symbol import sym_m
+    T = toeplitz_T(p, 30)
+    if p == 1:
+        assert np.array_equal(T, np.eye(30))
+        return
+    assert np.max(np.abs(T - T.T)) == 0.0
+    ev = np.linalg.eigvalsh(T)
+    assert ev.max() <= 1 + 1e-12 and ev.min() >= sym_m(p - 1, np.pi) - 1e-12
+    if p == 2:
+        assert abs(T[0, 0] - 2 / 3) < 1e-15 and abs(T[0, 1] - 1 / 6) < 1e-15
+    if p == 3:
+        assert abs(T[0, 0] - 11 / 20) < 1e-15
+
+
+def test_toeplitz_smoother_rho_and_fixed_point():
+    A, H = _setup(levels=2)
+    T = sp.kron(sp.identity(2), sp.kron(toeplitz_T(2, 8), toeplitz_T(2, 8))).toarray()
+    lam = sla.eigh(A.toarray(), T, eigvals_only=True)[-1]
+    assert 0.85 * lam <= H.rho_t[0] <= lam * (1 + 1e-10)
+    x = np.random.default_rng(2).standard_normal(A.shape[0])
+    assert np.max(np.abs(H.toeplitz(0, A @ x, x, 3) - x)) < 1e-12 * np.max(np.abs(x))

@@ -14,12 +14,13 @@ maxit = int(sys.argv[1]) if len(sys.argv) > 1 else 3000
 which = [int(a) for a in sys.argv[2:]] or [0, 1, 2, 3, 4]
 for ci in which:
     c = inputs.config(ci)
-    for mode in (ig.IGACD_PRECOND_AUX, ig.IGACD_PRECOND_VCYCLE):
+    for mode, sm in ((ig.IGACD_PRECOND_AUX, ig.IGACD_SMOOTH_TOEPLITZ), (ig.IGACD_PRECOND_AUX, ig.IGACD_SMOOTH_JACOBI)):
         t0 = time.time()
         h = ig.igacd_create(c.dim, c.p, c.n, c.nu, c.beta, c.lam, c.b0, levels=c.levels)
         torch.cuda.synchronize()
         t_setup = time.time() - t0
         ig.igacd_set_preconditioner(h, mode)
+        ig.igacd_set_smoother(h, sm)
         b = torch.from_numpy(inputs.rhs(c)).cuda()
         x = torch.zeros_like(b)
         torch.cuda.synchronize()
@@ -38,7 +39,7 @@ for ci in which:
         e1.record()
         torch.cuda.synchronize()
         ams = e0.elapsed_time(e1) / 10
-        print(json.dumps({"config": c.name, "precond": mode, "levels": ig.igacd_num_levels(h), "ndof": c.ndof,
+        print(json.dumps({"config": c.name, "precond": mode, "smoother": sm, "aux_exact": ig.igacd_aux_is_exact(h), "levels": ig.igacd_num_levels(h), "ndof": c.ndof,
                           "setup_s": round(t_setup, 3), "iters": it, "relres": rel, "solve_s": round(t_solve, 3),
                           "apply_ms": round(ams, 4), "apply_gdofs": round(c.ndof / ams / 1e6, 2),
                           "apply_gbs_alg": round(16 * c.ndof / ams / 1e6, 1),
