@@ -277,6 +277,8 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
       }
     const Coef coef = patterns(dim, mass, K);
     const std::vector<int> ns = level_sizes(dim, p, n, levels);
+    if ((double)dim * std::pow((double)(n + p - 2), dim) >= 2147483647.0)
+      throw Error{IGACD_E_ARG, "problem too large: d*m^d must stay below 2^31"};
     h->lv.resize(ns.size());
     for (size_t l = 0; l < ns.size(); ++l) {
       Level& L = h->lv[l];

@@ -12,6 +12,7 @@
 // pairing (one add feeds M and S, one subtract feeds A); threads whose row lies in the
 // boundary zone redo their contraction with the row's own band.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -225,20 +226,22 @@ struct Op3dShape {
   static constexpr int LPT = (NC * XS + NT - 1) / NT;
 };
 
-template <int P, int T2, int T3, int NC>
-__global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi ep, int mode, int dot,
-                                                 const double* __restrict__ x, double* __restrict__ y,
-                                                 int chunk) {
+template <int P, int T2, int T3, int NC, int MINB>
+__global__ void __launch_bounds__(T2* T3, MINB) k_op3d(const OpParams op, const Epi ep, int mode, int dot,
+                                                    const double* __restrict__ x, double* __restrict__ y,
+                                                    int chunk) {
   using Sh = Op3dShape<P, T2, T3, NC>;
   constexpr int NT = Sh::NT, R = Sh::R, HC = Sh::HC, XS = Sh::XS, US = Sh::US, LPT = Sh::LPT;
+  static_assert(T2 * HC <= 2 * NT, "stage A assumes at most two items per thread");
+  static_assert(LPT <= 32, "prefetch mask");
   extern __shared__ double smem[];
   double* xs = smem;                   // [2][NC][HR][HC]
   double* us = smem + 2 * NC * XS;     // [3][NC][T2][HC]: index (F*NC + j), F: 0 M, 1 S, 2 A
   double* wts = us + 3 * NC * US;      // [2][3R]
   double* red = wts + 2 * 3 * R;
   const int m = op.m;
-  const size_t ms = (size_t)m * m;
-  const size_t m3 = ms * m;
+  const int ms = m * m;                // ndof < 2^31 is checked on the host
+  const int m3 = ms * m;
   const int tid = threadIdx.x;
   const int tr = tid / T3, tc = tid % T3;
   const int r0 = blockIdx.y * T2, q0 = blockIdx.x * T3;
@@ -250,6 +253,33 @@ __global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi
   const int sb = max(0, c0 - P);
   const int se = c1 + P;
 
+  // ---- slab-invariant per-thread offsets -------------------------------------------------
+  int goff[LPT];          // global offset (without the slab term) of each prefetch slot
+  unsigned vmask = 0u;    // slot is inside the domain (in-plane)
+#pragma unroll
+  for (int i = 0; i < LPT; ++i) {
+    const int idx = tid + i * NT;
+    goff[i] = 0;
+    if (idx < NC * XS) {
+      const int j = idx / XS, rem = idx % XS;
+      const int g1 = r0 - P + rem / HC, g2 = q0 - P + rem % HC;
+      if (g1 >= 0 && g1 < m && g2 >= 0 && g2 < m) {
+        goff[i] = j * m3 + g1 * m + g2;
+        vmask |= 1u << i;
+      }
+    }
+  }
+  // stage A items: it0 = tid, it1 = tid + NT (when it exists)
+  const int it0 = tid, it1 = tid + NT;
+  const bool has1 = it1 < T2 * HC;
+  const int xo0 = (it0 / HC + P) * HC + it0 % HC;
+  const int xo1 = has1 ? (it1 / HC + P) * HC + it1 % HC : 0;
+  const int ga0 = r0 + it0 / HC, ga1 = r0 + it1 / HC;
+  const bool za0 = ga0 < m && (ga0 < op.zoneL || ga0 >= op.zoneR);
+  const bool za1 = has1 && ga1 < m && (ga1 < op.zoneL || ga1 >= op.zoneR);
+  const int bo = tr * HC + tc + P;     // stage-B window centre
+  const int pto = gr * m + gc;         // in-slab output offset
+
   double acc[NC][R];
 #pragma unroll
   for (int i = 0; i < NC; ++i)
@@ -257,20 +287,52 @@ __global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi
     for (int r = 0; r < R; ++r) acc[i][r] = 0.0;
   double dsum = 0.0;
 
-  // slab s -> xs[buf] by asynchronous copies (zero fill outside the domain)
   auto prefetch = [&](int s, int buf) {
+    double* dst = xs + buf * NC * XS + tid;
+    const bool sv = s < m;
+    const double* src = x + (size_t)s * ms;
 #pragma unroll
     for (int i = 0; i < LPT; ++i) {
-      const int idx = tid + i * NT;
-      if (idx < NC * XS) {
-        const int j = idx / XS, rem = idx % XS;
-        const int hr = rem / HC, hc = rem % HC;
-        const int g1 = r0 - P + hr, g2 = q0 - P + hc;
-        const bool ok = s < m && g1 >= 0 && g1 < m && g2 >= 0 && g2 < m;
-        cp_async8(xs + buf * NC * XS + idx, ok ? x + j * m3 + (size_t)s * ms + (size_t)g1 * m + g2 : x, ok);
+      if (tid + i * NT < NC * XS) {
+        const bool ok = sv && ((vmask >> i) & 1u);
+        cp_async8(dst + i * NT, ok ? src + goff[i] : x, ok);
       }
     }
     cp_async_commit();
+  };
+
+  // stage A on one item: contract direction 1 of x at (row, column) for all components
+  auto stageA = [&](const double* xb, int xo, int it, int g1, bool zone) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const double* xc_ = xb + j * XS + xo;
+      const double xc = xc_[0];
+      double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
+#pragma unroll
+      for (int o = 1; o <= P; ++o) {
+        const double lo = xc_[-o * HC], hi = xc_[o * HC];
+        const double sp = lo + hi, sm = hi - lo;
+        vm = fma(op.tM[o], sp, vm);
+        vs = fma(op.tS[o], sp, vs);
+        va = fma(op.tA[o], sm, va);
+      }
+      if (zone) {
+        const double* rM = op.bM + g1 * R + P;
+        const double* rS = op.bS + g1 * R + P;
+        const double* rA = op.bA + g1 * R + P;
+        vm = vs = va = 0.0;
+#pragma unroll
+        for (int o = -P; o <= P; ++o) {
+          const double v = xc_[o * HC];
+          vm = fma(__ldg(rM + o), v, vm);
+          vs = fma(__ldg(rS + o), v, vs);
+          va = fma(__ldg(rA + o), v, va);
+        }
+      }
+      us[(0 * NC + j) * US + it] = vm;
+      us[(1 * NC + j) * US + it] = vs;
+      us[(2 * NC + j) * US + it] = va;
+    }
   };
 
   prefetch(sb, 0);
@@ -286,43 +348,9 @@ __global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi
       load_col_weights<P>(op, s + 1, c0, c1, wts + (buf ^ 1) * 3 * R);
     }
     if (s < m) {
-      // ---- stage A: contract direction 1 for rows [0,T2) x halo columns [0,HC)
-#pragma unroll 1
-      for (int it = tid; it < T2 * HC; it += NT) {
-        const int r = it / HC, cc = it % HC;
-        const int g1 = r0 + r;
-        const bool zoneA = g1 < m && (g1 < op.zoneL || g1 >= op.zoneR);
-#pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          const double* xc_ = xs + buf * NC * XS + j * XS + (r + P) * HC + cc;
-          const double xc = xc_[0];
-          double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
-#pragma unroll
-          for (int o = 1; o <= P; ++o) {
-            const double lo = xc_[-o * HC], hi = xc_[o * HC];
-            const double sp = lo + hi, sm = hi - lo;
-            vm = fma(op.tM[o], sp, vm);
-            vs = fma(op.tS[o], sp, vs);
-            va = fma(op.tA[o], sm, va);
-          }
-          if (zoneA) {
-            const double* rM = op.bM + (size_t)g1 * R + P;
-            const double* rS = op.bS + (size_t)g1 * R + P;
-            const double* rA = op.bA + (size_t)g1 * R + P;
-            vm = vs = va = 0.0;
-#pragma unroll
-            for (int o = -P; o <= P; ++o) {
-              const double v = xc_[o * HC];
-              vm = fma(__ldg(rM + o), v, vm);
-              vs = fma(__ldg(rS + o), v, vs);
-              va = fma(__ldg(rA + o), v, va);
-            }
-          }
-          us[(0 * NC + j) * US + it] = vm;
-          us[(1 * NC + j) * US + it] = vs;
-          us[(2 * NC + j) * US + it] = va;
-        }
-      }
+      const double* xb = xs + buf * NC * XS;
+      stageA(xb, xo0, it0, ga0, za0);
+      if (has1) stageA(xb, xo1, it1, ga1, za1);
       __syncthreads();
       // ---- stage B: contract direction 2, combine patterns into z_{i,F0}
       double zM[NC], zS[NC], zA[NC];
@@ -330,9 +358,9 @@ __global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi
       for (int i = 0; i < NC; ++i) zM[i] = zS[i] = zA[i] = 0.0;
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
-        const double* uM = us + (0 * NC + j) * US + tr * HC + tc + P;
-        const double* uS = us + (1 * NC + j) * US + tr * HC + tc + P;
-        const double* uA = us + (2 * NC + j) * US + tr * HC + tc + P;
+        const double* uM = us + (0 * NC + j) * US + bo;
+        const double* uS = us + (1 * NC + j) * US + bo;
+        const double* uA = us + (2 * NC + j) * US + bo;
         double vMM, vMS, vMA, vSM, vAM, vAA;
         {
           const double c = uM[0];
@@ -365,9 +393,9 @@ __global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi
           vAM = a1; vAA = a3;
         }
         if (zoneB) {
-          const double* rM = op.bM + (size_t)gc * R + P;
-          const double* rS = op.bS + (size_t)gc * R + P;
-          const double* rA = op.bA + (size_t)gc * R + P;
+          const double* rM = op.bM + gc * R + P;
+          const double* rS = op.bS + gc * R + P;
+          const double* rA = op.bA + gc * R + P;
           vMM = vMS = vMA = vSM = vAM = vAA = 0.0;
 #pragma unroll
           for (int o = -P; o <= P; ++o) {
@@ -403,14 +431,14 @@ __global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi
     {
       const int t = s - P;
       if (t >= c0 && t < c1 && active) {
-        const size_t pt = (size_t)t * ms + (size_t)gr * m + gc;
+        const int pt = t * ms + pto;
         double Dv[NC];
 #pragma unroll
         for (int i = 0; i < NC; ++i) Dv[i] = 1.0;
         if (mode >= EPI_JACOBI) {
-          const double M0 = __ldg(op.bM + (size_t)t * R + P), S0 = __ldg(op.bS + (size_t)t * R + P);
-          const double M1 = __ldg(op.bM + (size_t)gr * R + P), S1 = __ldg(op.bS + (size_t)gr * R + P);
-          const double M2 = __ldg(op.bM + (size_t)gc * R + P), S2 = __ldg(op.bS + (size_t)gc * R + P);
+          const double M0 = __ldg(op.bM + t * R + P), S0 = __ldg(op.bS + t * R + P);
+          const double M1 = __ldg(op.bM + gr * R + P), S1 = __ldg(op.bS + gr * R + P);
+          const double M2 = __ldg(op.bM + gc * R + P), S2 = __ldg(op.bS + gc * R + P);
 #pragma unroll
           for (int i = 0; i < NC; ++i)
             Dv[i] = op.c.mass[i][i] * M0 * M1 * M2 + op.c.S[0][i][i] * S0 * M1 * M2 +
@@ -419,7 +447,7 @@ __global__ void __launch_bounds__(T2* T3, 2) k_op3d(const OpParams op, const Epi
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
           const double a = acc[i][0];
-          const size_t gi = (size_t)i * m3 + pt;
+          const int gi = i * m3 + pt;
           double out;
           if (mode == EPI_APPLY) out = a;
           else if (mode == EPI_RESID) out = ep.b[gi] - a;
@@ -472,7 +500,7 @@ static Grid grid_for(const Handle& h, int level) {
     const int tx = (m + NT2D - 1) / NT2D;
     int nch = std::max(1, std::min(m, (TARGET_CTAS + tx - 1) / tx));
     g.chunk = (m + nch - 1) / nch;
-    g.chunk = std::max(g.chunk, std::min(m, 4 * h.p));
+    g.chunk = std::max(g.chunk, std::min(m, 2 * h.p + 1));
     nch = (m + g.chunk - 1) / g.chunk;
     g.grid = dim3(tx, nch, 1);
   } else {
@@ -497,17 +525,33 @@ static void launch2d(const Grid& g, const OpParams& op, const Epi& ep, int mode,
   k_op2d<P, NT2D, NC><<<g.grid, NT2D, 0, s>>>(op, ep, mode, dot, x, y, g.chunk);
 }
 
-template <int P, int NC>
-static void launch3d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
-                     cudaStream_t s) {
+static int minb_choice() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IGACD_MINB");
+    v = (e && e[0] == '1') ? 1 : 2;
+  }
+  return v;
+}
+
+template <int P, int NC, int MINB>
+static void launch3d_m(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                       cudaStream_t s) {
   using Sh = Op3dShape<P, T2_3D, T3_3D, NC>;
   static bool attr = false;
   if (!attr) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_op3d<P, T2_3D, T3_3D, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    IGACD_CUDA(cudaFuncSetAttribute(k_op3d<P, T2_3D, T3_3D, NC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     Sh::SMEM));
     attr = true;
   }
-  k_op3d<P, T2_3D, T3_3D, NC><<<g.grid, Sh::NT, Sh::SMEM, s>>>(op, ep, mode, dot, x, y, g.chunk);
+  k_op3d<P, T2_3D, T3_3D, NC, MINB><<<g.grid, Sh::NT, Sh::SMEM, s>>>(op, ep, mode, dot, x, y, g.chunk);
+}
+
+template <int P, int NC>
+static void launch3d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                     cudaStream_t s) {
+  if (minb_choice() == 1) launch3d_m<P, NC, 1>(g, op, ep, mode, dot, x, y, s);
+  else launch3d_m<P, NC, 2>(g, op, ep, mode, dot, x, y, s);
 }
 
 template <int P>
