@@ -67,6 +67,118 @@ __global__ void k_band_solve(double* __restrict__ data, long long outer, int m, 
   }
 }
 
+__device__ __forceinline__ void ls_cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gsrc) : "memory");
+}
+
+// Tiled variant: each warp stages 32 lines in shared memory (coalesced loads/stores), and
+// every lane runs its substitution out of shared memory, so the sequential recurrence sees
+// shared-memory latency instead of DRAM latency.  Requires inner == 1 or inner % 32 == 0.
+template <int W, int WARPS, int TW>
+__global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restrict__ data, long long outer, int m,
+                                                               long long inner, const double* __restrict__ Lb,
+                                                               const double* __restrict__ inv, int mode,
+                                                               double omega, double* __restrict__ xacc) {
+  extern __shared__ double sh[];
+  double* sL = sh;                          // [m][W+1]
+  double* sI = sL + (size_t)m * (W + 1);    // [m]
+  constexpr int TP = TW + 1;                // padded tile row (bank-conflict free for TW = 32)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* tile = sI + m + (size_t)warp * m * TP;   // [m][TP]
+  for (int i = threadIdx.x; i < m * (W + 1); i += blockDim.x) sL[i] = Lb[i];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) sI[i] = inv[i];
+  __syncthreads();
+  const long long lines = outer * inner;
+  const long long groups = (lines + TW - 1) / TW;
+  for (long long g = (long long)blockIdx.x * WARPS + warp; g < groups; g += (long long)gridDim.x * WARPS) {
+    const long long l0 = g * TW;
+    const int nl = (int)min((long long)TW, lines - l0);
+    // ---- load the TW x m tile with asynchronous copies (all loads in flight at once)
+    if (inner == 1) {
+      const double* src = data + l0 * m;
+      for (int e = lane; e < nl * m; e += 32) ls_cp_async8(&tile[(e % m) * TP + e / m], src + e);
+    } else {   // lanes = consecutive lines: coalesced except where the group crosses an `outer` step
+      const long long l = l0 + lane;
+      const double* src = data + (l / inner) * (long long)m * inner + (l % inner);
+      if (lane < nl)
+        for (int k = 0; k < m; ++k) ls_cp_async8(&tile[k * TP + lane], src + (long long)k * inner);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+    if (lane < nl) {
+      double win[W + 1];
+#pragma unroll
+      for (int j = 0; j <= W; ++j) win[j] = 0.0;
+      for (int k = 0; k < m; ++k) {
+#pragma unroll
+        for (int j = W; j >= 1; --j) win[j] = win[j - 1];
+        double acc = tile[k * TP + lane];
+        const double* Lr = sL + (size_t)k * (W + 1);
+#pragma unroll
+        for (int j = 1; j <= W; ++j) acc = fma(-Lr[W - j], win[j], acc);
+        win[0] = acc * sI[k];
+        tile[k * TP + lane] = win[0];
+      }
+#pragma unroll
+      for (int j = 0; j <= W; ++j) win[j] = 0.0;
+      for (int k = m - 1; k >= 0; --k) {
+#pragma unroll
+        for (int j = W; j >= 1; --j) win[j] = win[j - 1];
+        double acc = tile[k * TP + lane];
+#pragma unroll
+        for (int j = 1; j <= W; ++j)
+          if (k + j < m) acc = fma(-sL[(size_t)(k + j) * (W + 1) + W - j], win[j], acc);
+        win[0] = acc * sI[k];
+        tile[k * TP + lane] = win[0];
+      }
+    }
+    __syncwarp();
+    // ---- store (or accumulate omega * result into xacc, reading xacc 8 elements ahead so the
+    // read-modify-writes overlap instead of serialising on DRAM latency)
+    constexpr int U = 8;
+    if (inner == 1) {
+      double* dst = (mode == 0 ? data : xacc) + l0 * m;
+      const int tot = nl * m;
+      for (int e0 = lane; e0 < tot; e0 += 32 * U) {
+        double xv[U];
+        if (mode != 0) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) xv[u] = (e0 + 32 * u < tot) ? dst[e0 + 32 * u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + 32 * u;
+          if (e < tot) {
+            const double v = tile[(e % m) * TP + e / m];
+            dst[e] = mode == 0 ? v : fma(omega, v, xv[u]);
+          }
+        }
+      }
+    } else {
+      const long long l = l0 + lane;
+      double* dst = (mode == 0 ? data : xacc) + (l / inner) * (long long)m * inner + (l % inner);
+      if (lane < nl)
+        for (int k0 = 0; k0 < m; k0 += U) {
+          double xv[U];
+          if (mode != 0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = (k0 + u < m) ? dst[(long long)(k0 + u) * inner] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int k = k0 + u;
+            if (k < m) {
+              const double v = tile[k * TP + lane];
+              dst[(long long)k * inner] = mode == 0 ? v : fma(omega, v, xv[u]);
+            }
+          }
+        }
+    }
+    __syncwarp();
+  }
+}
+
 // banded Cholesky on the host: F given in band storage [m][2w+1] (F[k][k+o] at k*(2w+1)+o+w)
 void band_cholesky(const std::vector<double>& F, int m, int w, std::vector<double>& Lb, std::vector<double>& inv) {
   Lb.assign((size_t)m * (w + 1), 0.0);
@@ -103,9 +215,33 @@ void BandFactor::release() {
   Lb = inv = nullptr;
 }
 
+template <int W, int WARPS, int TW>
+static bool try_tiled(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode,
+                      double omega, double* xacc, cudaStream_t s) {
+  const size_t smem_t = sizeof(double) * ((size_t)m * (W + 1) + m + (size_t)WARPS * m * (TW + 1));
+  if (smem_t > 200 * 1024) return false;
+  static size_t attr_t = 0;
+  if (smem_t > 48 * 1024 && attr_t < smem_t) {
+    IGACD_CUDA(cudaFuncSetAttribute(k_band_solve_tiled<W, WARPS, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem_t));
+    attr_t = smem_t;
+  }
+  const long long groups = (outer * inner + TW - 1) / TW;
+  long long blocks = (groups + WARPS - 1) / WARPS;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_band_solve_tiled<W, WARPS, TW><<<(unsigned)blocks, 32 * WARPS, smem_t, s>>>(data, outer, m, inner, F.Lb, F.inv,
+                                                                              mode, omega, xacc);
+  return true;
+}
+
 template <int W>
 static void launch_w(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode,
                      double omega, double* xacc, cudaStream_t s) {
+  // widest tile that fits: 32 lines per warp (2 warps), else 16 or 8 lines (1 warp)
+  if (try_tiled<W, 2, 32>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  if (try_tiled<W, 1, 32>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  if (try_tiled<W, 1, 16>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  if (try_tiled<W, 1, 8>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
   const size_t smem = sizeof(double) * ((size_t)m * (W + 1) + m);
   static int attr_set = 0;
   if (smem > 48 * 1024 && attr_set < (int)smem) {

@@ -3,40 +3,66 @@
 // direction.  Each pass views the array as [outer][axis][inner] and writes one output
 // element per thread from the fixed-width row storage of P (or P^T): coalesced along
 // `inner`, and for the fastest axis consecutive threads read overlapping windows.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace igacd {
 
-__global__ void k_axis_pass(const double* __restrict__ in, double* __restrict__ out, long long outer, int nin,
-                            int nout, long long inner, const int* __restrict__ start,
-                            const double* __restrict__ w, int W, int accumulate) {
-  const long long total = outer * nout * inner;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long in_ = idx % inner;
-    const long long t = idx / inner;
-    const int o = (int)(t % nout);
-    const long long ou = t / nout;
+// inner == 1 (fastest axis): one output per thread, 32-bit index math
+__global__ void k_axis_pass_fast(const double* __restrict__ in, double* __restrict__ out, int outer, int nin, int nout,
+                                 const int* __restrict__ start, const double* __restrict__ w, int W, int accumulate) {
+  const int total = outer * nout;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int o = idx % nout, ou = idx / nout;
     const int st = __ldg(start + o);
-    const double* src = in + (ou * nin + st) * inner + in_;
-    const double* wr = w + (size_t)o * W;
+    const double* src = in + ou * nin + st;
+    const double* wr = w + o * W;
     double acc = 0.0;
-    for (int k = 0; k < W; ++k) {
-      if (st + k < nin) acc = fma(__ldg(wr + k), __ldg(src + (long long)k * inner), acc);
-    }
+    for (int k = 0; k < W; ++k)
+      if (st + k < nin) acc = fma(__ldg(wr + k), __ldg(src + k), acc);
     if (accumulate) out[idx] += acc;
     else out[idx] = acc;
   }
 }
 
+// inner > 1: blockIdx.y = output row (ou, o), threads along the contiguous inner index
+__global__ void k_axis_pass_rows(const double* __restrict__ in, double* __restrict__ out, int rows, int nin, int nout,
+                                 int inner, const int* __restrict__ start, const double* __restrict__ w, int W,
+                                 int accumulate) {
+  const int row = blockIdx.y + blockIdx.z * gridDim.y;
+  if (row >= rows) return;
+  const int o = row % nout, ou = row / nout;
+  const int st = __ldg(start + o);
+  const double* wr = w + o * W;
+  const double* src = in + ((long long)ou * nin + st) * inner;
+  double* dst = out + (long long)row * inner;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < inner; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < W; ++k)
+      if (st + k < nin) acc = fma(__ldg(wr + k), __ldg(src + (long long)k * inner + i), acc);
+    if (accumulate) dst[i] += acc;
+    else dst[i] = acc;
+  }
+}
+
 static void axis_pass(Handle& h, const double* in, double* out, long long outer, int nin, int nout, long long inner,
                       const int* start, const double* w, int W, bool acc, cudaStream_t s) {
-  const long long total = outer * nout * inner;
   const int bs = 256;
-  long long blocks = (total + bs - 1) / bs;
-  if (blocks > 148LL * 16) blocks = 148LL * 16;
-  if (blocks < 1) blocks = 1;
-  k_axis_pass<<<(unsigned)blocks, bs, 0, s>>>(in, out, outer, nin, nout, inner, start, w, W, acc ? 1 : 0);
+  if (inner == 1) {
+    const long long total = outer * nout;
+    long long blocks = (total + bs - 1) / bs;
+    if (blocks > 148LL * 16) blocks = 148LL * 16;
+    k_axis_pass_fast<<<(unsigned)std::max(1LL, blocks), bs, 0, s>>>(in, out, (int)outer, nin, nout, start, w, W,
+                                                                    acc ? 1 : 0);
+  } else {
+    const long long rows = outer * nout;
+    const int gy = (int)std::min(rows, 65535LL);
+    const int gz = (int)((rows + gy - 1) / gy);
+    const int gx = (int)std::min((inner + bs - 1) / bs, 65535LL);
+    k_axis_pass_rows<<<dim3(gx, gy, gz), bs, 0, s>>>(in, out, (int)rows, nin, nout, (int)inner, start, w, W,
+                                                     acc ? 1 : 0);
+  }
   IGACD_LAUNCH_CHECK();
   count_launch(h);
 }
