@@ -127,6 +127,7 @@ struct Handle {
   // PCG / preconditioner vectors (level-0 size)
   double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *px = nullptr, *pb = nullptr;
   double *aw = nullptr, *ar = nullptr;   // aux preconditioner work (level-0 vector size)
+  double* zbuf = nullptr;                // 3D split operator: 3*nc per-point combinations (level-0 size)
   cudaStream_t stream = nullptr;
   // instrumentation
   long long launches = 0, apply_launches = 0;
@@ -161,7 +162,8 @@ void gauss_legendre(int q, double* x01, double* w01);
 // (0 if dot == DOT_NONE)
 int launch_operator(Handle& h, int sy, int level, const double* x, double* out, EpiMode mode, DotMode dot,
                     const Epi& epi, cudaStream_t s);
-int operator_ctas(const Handle& h, int level);
+int operator_ctas(const Handle& h, int level);                  // max over both systems
+int operator_ctas_sys(const Handle& h, int level, int nc);
 
 // ---- transfer.cu --------------------------------------------------------------------
 void launch_prolong(Handle& h, int nc, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s);
