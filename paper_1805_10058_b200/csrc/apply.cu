@@ -1089,6 +1089,203 @@ __global__ void __launch_bounds__(T2* T3) k_slab3d(const OpParams op, const doub
   }
 }
 
+// (S2): as k_slab3d, but each thread forms TWO adjacent outputs along direction 2 from one
+// window of 2P+2 values read as 16-byte pairs (LDS.128): 44% fewer shared-memory wavefronts
+// in stage B, which dominated the slab kernel's shared-memory traffic.
+template <int P, int T2, int T3, int NC>
+struct Slab2Shape {
+  static constexpr int TC = T3 / 2;             // threads per row
+  static constexpr int NT = T2 * TC;
+  static constexpr int HR = T2 + 2 * P;
+  static constexpr int HC = T3 + 2 * P;         // even: rows stay 16-byte aligned
+  static constexpr int XS = HR * HC;
+  static constexpr int US = T2 * HC;
+  static constexpr int SMEM = (NC * XS + 3 * NC * US) * 8;
+  static constexpr int LPT = (NC * XS + NT - 1) / NT;
+};
+
+template <int P, int T2, int T3, int NC>
+__global__ void __launch_bounds__(T2*(T3 / 2)) k_slab3d2(const OpParams op, const double* __restrict__ x,
+                                                         double* __restrict__ Z) {
+  using Sh = Slab2Shape<P, T2, T3, NC>;
+  constexpr int NT = Sh::NT, R = 2 * P + 1, HC = Sh::HC, XS = Sh::XS, US = Sh::US, LPT = Sh::LPT, TC = Sh::TC;
+  constexpr int RH = T2 / 2;
+  constexpr int WN = 2 * P + 2;
+  extern __shared__ __align__(16) double smem[];
+  double* xs = smem;               // [NC][HR][HC]
+  double* us = smem + NC * XS;     // [3][NC][T2][HC]
+  const int m = op.m;
+  const int ms = m * m, m3 = ms * m;
+  const int s = blockIdx.z;
+  const int tid = threadIdx.x;
+  const int tr = tid / TC, tc = tid % TC;
+  const int r0 = blockIdx.y * T2, q0 = blockIdx.x * T3;
+  const int gr = r0 + tr, gc0 = q0 + 2 * tc;
+  const bool act0 = gr < m && gc0 < m, act1 = gr < m && gc0 + 1 < m;
+  const bool zb0 = act0 && (gc0 < op.zoneL || gc0 >= op.zoneR);
+  const bool zb1 = act1 && (gc0 + 1 < op.zoneL || gc0 + 1 >= op.zoneR);
+  const bool wzb = __any_sync(0xffffffffu, zb0 || zb1);
+  const double* src = x + (size_t)s * ms;
+#pragma unroll
+  for (int i = 0; i < LPT; ++i) {
+    const int idx = tid + i * NT;
+    if (idx < NC * XS) {
+      const int j = idx / XS, rem = idx % XS;
+      const int g1 = r0 - P + rem / HC, g2 = q0 - P + rem % HC;
+      const bool ok = g1 >= 0 && g1 < m && g2 >= 0 && g2 < m;
+      cp_async8(xs + idx, ok ? src + j * m3 + g1 * m + g2 : x, ok);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- stage A: direction 1 (as in k_slab3d)
+  for (int it = tid; it < 2 * NC * HC; it += NT) {
+    const int a_cc = it % HC, a_j = (it / HC) % NC, a_r0 = (it / (NC * HC)) * RH;
+    const double* col = xs + a_j * XS + a_r0 * HC + a_cc;
+    double win[RH + 2 * P];
+#pragma unroll
+    for (int k = 0; k < RH + 2 * P; ++k) win[k] = col[k * HC];
+    const int g0 = r0 + a_r0;
+    const bool zone_any = g0 < op.zoneL || g0 + RH > op.zoneR;
+#pragma unroll
+    for (int r = 0; r < RH; ++r) {
+      const double xc = win[r + P];
+      double vm = op.tM[0] * xc, vs = op.tS[0] * xc, va = 0.0;
+#pragma unroll
+      for (int o = 1; o <= P; ++o) {
+        const double lo = win[r + P - o], hi = win[r + P + o];
+        const double sp = lo + hi, sm = hi - lo;
+        vm = fma(op.tM[o], sp, vm);
+        vs = fma(op.tS[o], sp, vs);
+        va = fma(op.tA[o], sm, va);
+      }
+      if (zone_any) {
+        const int g1 = g0 + r;
+        if (g1 < m && (g1 < op.zoneL || g1 >= op.zoneR)) {
+          const double* rM = op.bM + g1 * R + P;
+          const double* rS = op.bS + g1 * R + P;
+          const double* rA = op.bA + g1 * R + P;
+          vm = vs = va = 0.0;
+#pragma unroll
+          for (int o = -P; o <= P; ++o) {
+            const double v = win[r + P + o];
+            vm = fma(__ldg(rM + o), v, vm);
+            vs = fma(__ldg(rS + o), v, vs);
+            va = fma(__ldg(rA + o), v, va);
+          }
+        }
+      }
+      const int uo = (a_r0 + r) * HC + a_cc;
+      us[(0 * NC + a_j) * US + uo] = vm;
+      us[(1 * NC + a_j) * US + uo] = vs;
+      us[(2 * NC + a_j) * US + uo] = va;
+    }
+  }
+  __syncthreads();
+  if (!act0) return;
+  // ---- stage B: direction 2 for the pair (gc0, gc0 + 1) and the pattern combinations
+  double zM[2][NC], zS[2][NC], zA[2][NC];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int i = 0; i < NC; ++i) zM[q][i] = zS[q][i] = zA[q][i] = 0.0;
+  const int bo = tr * HC + 2 * tc;   // window start: column gc0 - P
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    double wM[WN], wS[WN], wA[WN];
+    {
+      const double2* pM = reinterpret_cast<const double2*>(us + (0 * NC + j) * US + bo);
+      const double2* pS = reinterpret_cast<const double2*>(us + (1 * NC + j) * US + bo);
+      const double2* pA = reinterpret_cast<const double2*>(us + (2 * NC + j) * US + bo);
+#pragma unroll
+      for (int k = 0; k < WN / 2; ++k) {
+        const double2 a = pM[k], b = pS[k], c = pA[k];
+        wM[2 * k] = a.x; wM[2 * k + 1] = a.y;
+        wS[2 * k] = b.x; wS[2 * k + 1] = b.y;
+        wA[2 * k] = c.x; wA[2 * k + 1] = c.y;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double* uM = wM + P + q;   // centre of point q
+      const double* uS = wS + P + q;
+      const double* uA = wA + P + q;
+      double vMM, vMS, vMA, vSM, vAM, vAA;
+      {
+        const double c = uM[0];
+        double a1 = op.tM[0] * c, a2 = op.tS[0] * c, a3 = 0.0;
+#pragma unroll
+        for (int o = 1; o <= P; ++o) {
+          const double lo = uM[-o], hi = uM[o];
+          const double sp = lo + hi, sm = hi - lo;
+          a1 = fma(op.tM[o], sp, a1);
+          a2 = fma(op.tS[o], sp, a2);
+          a3 = fma(op.tA[o], sm, a3);
+        }
+        vMM = a1; vMS = a2; vMA = a3;
+      }
+      {
+        double a1 = op.tM[0] * uS[0];
+#pragma unroll
+        for (int o = 1; o <= P; ++o) a1 = fma(op.tM[o], uS[-o] + uS[o], a1);
+        vSM = a1;
+      }
+      {
+        const double c = uA[0];
+        double a1 = op.tM[0] * c, a3 = 0.0;
+#pragma unroll
+        for (int o = 1; o <= P; ++o) {
+          const double lo = uA[-o], hi = uA[o];
+          a1 = fma(op.tM[o], lo + hi, a1);
+          a3 = fma(op.tA[o], hi - lo, a3);
+        }
+        vAM = a1; vAA = a3;
+      }
+      const bool zb = q == 0 ? zb0 : zb1;
+      if (wzb && zb) {
+        const int g = gc0 + q;
+        const double* rM = op.bM + g * R + P;
+        const double* rS = op.bS + g * R + P;
+        const double* rA = op.bA + g * R + P;
+        vMM = vMS = vMA = vSM = vAM = vAA = 0.0;
+#pragma unroll
+        for (int o = -P; o <= P; ++o) {
+          const double wm = __ldg(rM + o), ws = __ldg(rS + o), wa = __ldg(rA + o);
+          vMM = fma(wm, uM[o], vMM);
+          vMS = fma(ws, uM[o], vMS);
+          vMA = fma(wa, uM[o], vMA);
+          vSM = fma(wm, uS[o], vSM);
+          vAM = fma(wm, uA[o], vAM);
+          vAA = fma(wa, uA[o], vAA);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        zM[q][i] = fma(op.c.mass[i][j], vMM, zM[q][i]);
+        zS[q][i] = fma(op.c.S[0][i][j], vMM, zS[q][i]);
+        zM[q][i] = fma(op.c.S[1][i][j], vSM, zM[q][i]);
+        zM[q][i] = fma(op.c.S[2][i][j], vMS, zM[q][i]);
+        zA[q][i] = fma(op.c.AA[0][i][j], vAM, zA[q][i]);
+        zA[q][i] = fma(op.c.AA[1][i][j], vMA, zA[q][i]);
+        zM[q][i] = fma(op.c.AA[2][i][j], vAA, zM[q][i]);
+      }
+    }
+  }
+  const int pt = s * ms + gr * m + gc0;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    Z[(size_t)(0 * NC + i) * m3 + pt] = zM[0][i];
+    Z[(size_t)(1 * NC + i) * m3 + pt] = zS[0][i];
+    Z[(size_t)(2 * NC + i) * m3 + pt] = zA[0][i];
+    if (act1) {
+      Z[(size_t)(0 * NC + i) * m3 + pt + 1] = zM[1][i];
+      Z[(size_t)(1 * NC + i) * m3 + pt + 1] = zS[1][i];
+      Z[(size_t)(2 * NC + i) * m3 + pt + 1] = zA[1][i];
+    }
+  }
+}
+
 // (C): thread per (i2, i3) column; march s over the chunk; epilogue as in the fused kernels
 template <int P, int NC>
 __global__ void __launch_bounds__(256) k_col3d(const OpParams op, const Epi ep, int mode, int dot,
@@ -1213,13 +1410,19 @@ constexpr int T2_3D = 8, T3_3D = 32;      // k_op3d: one output point per thread
 constexpr int T2_3D2 = 8, T3_3D2 = 64;    // k_op3d2: two output points per thread
 constexpr int TARGET_CTAS = 4 * 148;
 
-static int split3d() {   // 3D operator as slab kernel + column kernel (default) or fused marching kernel
+static int split3d_mode() {   // IGACD_SPLIT: 0 fused only, 1 split for the vector system, 2 split for both
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("IGACD_SPLIT");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
   }
   return v;
+}
+
+// 3D operator as slab kernel + column kernel, or the fused marching kernel
+static bool use_split(int dim, int nc) {
+  const int v = split3d_mode();
+  return dim == 3 && (v == 2 || (v == 1 && nc == 3));
 }
 
 static int col_chunks(int m) {   // direction-0 chunks of the column kernel: >= ~4 CTAs per SM
@@ -1271,7 +1474,7 @@ int operator_ctas(const Handle& h, int level) {
 }
 
 int operator_ctas_sys(const Handle& h, int level, int nc) {
-  if (h.dim == 3 && split3d() && nc == 3) {
+  if (use_split(h.dim, nc)) {
     const int m = h.lv[level].m;
     const int chunk = col_chunks(m);
     return ((m * m + 255) / 256) * ((m + chunk - 1) / chunk);
@@ -1280,17 +1483,40 @@ int operator_ctas_sys(const Handle& h, int level, int nc) {
   return g.grid.x * g.grid.y * g.grid.z;
 }
 
+static int slab_variant() {   // IGACD_SLAB: 1 one point per thread (default), 2 two points per thread
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IGACD_SLAB");
+    v = (e && e[0] == '2') ? 2 : 1;
+  }
+  return v;
+}
+
+constexpr int T2_SL2 = 16, T3_SL2 = 32;
+
 template <int P, int NC>
 static void launch_split3d(const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
                            double* Z, cudaStream_t s) {
-  using Sh = SlabShape<P, 8, 32, NC>;
-  static bool attr = false;
-  if (!attr) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_slab3d<P, 8, 32, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM));
-    attr = true;
-  }
   const int m = op.m;
-  k_slab3d<P, 8, 32, NC><<<dim3((m + 31) / 32, (m + 7) / 8, m), Sh::NT, Sh::SMEM, s>>>(op, x, Z);
+  if (slab_variant() == 2) {
+    using Sh = Slab2Shape<P, T2_SL2, T3_SL2, NC>;
+    static bool attr2 = false;
+    if (!attr2) {
+      IGACD_CUDA(cudaFuncSetAttribute(k_slab3d2<P, T2_SL2, T3_SL2, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Sh::SMEM));
+      attr2 = true;
+    }
+    k_slab3d2<P, T2_SL2, T3_SL2, NC><<<dim3((m + T3_SL2 - 1) / T3_SL2, (m + T2_SL2 - 1) / T2_SL2, m), Sh::NT, Sh::SMEM,
+                                       s>>>(op, x, Z);
+  } else {
+    using Sh = SlabShape<P, 8, 32, NC>;
+    static bool attr = false;
+    if (!attr) {
+      IGACD_CUDA(cudaFuncSetAttribute(k_slab3d<P, 8, 32, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM));
+      attr = true;
+    }
+    k_slab3d<P, 8, 32, NC><<<dim3((m + 31) / 32, (m + 7) / 8, m), Sh::NT, Sh::SMEM, s>>>(op, x, Z);
+  }
   const int chunk = col_chunks(m);
   k_col3d<P, NC><<<dim3((m * m + 255) / 256, (m + chunk - 1) / chunk), 256, 0, s>>>(op, ep, mode, dot, Z, x, y,
                                                                                  chunk);
@@ -1417,8 +1643,9 @@ static void launch3d(const Grid& g, const OpParams& op, const Epi& ep, int mode,
 template <int P>
 static void dispatch(int dim, int nc, const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot,
                      const double* x, double* y, double* Z, cudaStream_t s) {
-  if (dim == 3 && split3d() && nc == 3) {   // the scalar (nc = 1) split launch faulted for p >= 3 in round 1
-    launch_split3d<P, 3>(op, ep, mode, dot, x, y, Z, s);
+  if (use_split(dim, nc)) {
+    if (nc == 1) launch_split3d<P, 1>(op, ep, mode, dot, x, y, Z, s);
+    else launch_split3d<P, 3>(op, ep, mode, dot, x, y, Z, s);
     return;
   }
   if (dim == 2) {
@@ -1448,7 +1675,7 @@ int launch_operator(Handle& h, int sy, int level, const double* x, double* out, 
   }
   IGACD_LAUNCH_CHECK();
   count_launch(h);
-  if (h.dim == 3 && split3d() && S.nc == 3) count_launch(h);
+  if (use_split(h.dim, S.nc)) count_launch(h);
   return dot != DOT_NONE ? nct : 0;
 }
 

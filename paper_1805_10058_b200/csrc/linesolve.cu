@@ -72,74 +72,155 @@ __device__ __forceinline__ void ls_cp_async8(double* smem_dst, const double* gsr
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gsrc) : "memory");
 }
 
-// Tiled variant: each warp stages 32 lines in shared memory (coalesced loads/stores), and
+// One substitution sweep over a line held in shared memory (element k at tile[k*TP + lane]),
+// in right-looking (column) order: when v_t is final it is scattered into the W pending rows,
+//   acc[q] (row t+1+q) -= G[t][q] v_t,  q = 0..W-1,
+// where forward G[t][q] = i_r L[r][t] (r = t+1+q) and backward G[t][q] = i_r L[k][r]
+// (k = m-1-t, r = k-1-q), and row t+W enters the ring as i_r * tile[r].  The loop-carried
+// dependency is one DFMA per step (acc[1] - G v_t -> next v).  Steps run in blocks of D (a
+// multiple of W, so the ring maps back onto itself); the shared-memory operands of block b+1
+// are loaded into the other of two register sets while block b is processed.
+template <int W>
+struct SweepSet {
+  static constexpr int D = W >= 3 ? W : W * ((4 + W - 1) / W);
+  double g[D][W], tv[D], iv[D];
+};
+
+// tile and sI carry W zero rows below 0 and above m-1, so the entering row t+W needs no guard
+template <int W, int TP, bool FWD>
+__device__ __forceinline__ void sweep_load(SweepSet<W>& S, const double* tile, const double* __restrict__ G,
+                                           const double* sI, int m, int t0) {
+  constexpr int D = SweepSet<W>::D;
+  const int r0 = FWD ? t0 + W : m - 1 - t0 - W;
+  const double* tb = tile + r0 * TP;
+  const double* ib = sI + r0;
+  const double* gb = G + t0 * (W + 1);
+#pragma unroll
+  for (int u = 0; u < D; ++u) {
+#pragma unroll
+    for (int q = 0; q < W; ++q) S.g[u][q] = gb[u * (W + 1) + q];
+    S.tv[u] = tb[FWD ? u * TP : -u * TP];
+    S.iv[u] = ib[FWD ? u : -u];
+  }
+}
+
+template <int W, int TP, bool FWD>
+__device__ __forceinline__ void sweep_block(const SweepSet<W>& S, double (&acc)[W], double* tile, int m, int t0) {
+  constexpr int D = SweepSet<W>::D;
+  double* tb = tile + (FWD ? t0 : m - 1 - t0) * TP;
+#pragma unroll
+  for (int u = 0; u < D; ++u) {
+    const double v = acc[0];
+    const double enter = S.tv[u] * S.iv[u];
+#pragma unroll
+    for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-S.g[u][q], v, acc[q + 1]);
+    acc[W - 1] = fma(-S.g[u][W - 1], v, enter);
+    tb[FWD ? u * TP : -u * TP] = v;
+  }
+}
+
+// `tile` points at this lane's element 0 (stride TP); `sI` at 1/L[0][0]; both padded by W zero rows
+template <int W, int TP, bool FWD>
+__device__ __forceinline__ void band_sweep(double* tile, const double* __restrict__ G, const double* sI, int m) {
+  auto row = [&](int t) { return FWD ? t : m - 1 - t; };
+  if constexpr (W == 0) {
+    for (int t = 0; t < m; ++t) tile[t * TP] *= sI[t];
+  } else {
+    constexpr int D = SweepSet<W>::D;
+    double acc[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) acc[q] = tile[row(q) * TP] * sI[row(q)];
+    const int nb = m / D;
+    SweepSet<W> s0, s1;
+    if (nb > 0) sweep_load<W, TP, FWD>(s0, tile, G, sI, m, 0);
+    for (int b = 0; b < nb; b += 2) {
+      if (b + 1 < nb) sweep_load<W, TP, FWD>(s1, tile, G, sI, m, (b + 1) * D);
+      sweep_block<W, TP, FWD>(s0, acc, tile, m, b * D);
+      if (b + 1 >= nb) break;
+      if (b + 2 < nb) sweep_load<W, TP, FWD>(s0, tile, G, sI, m, (b + 2) * D);
+      sweep_block<W, TP, FWD>(s1, acc, tile, m, (b + 1) * D);
+    }
+    for (int t = nb * D; t < m; ++t) {   // tail: fewer than D steps
+      const double v = acc[0];
+      const double enter = tile[row(t + W) * TP] * sI[row(t + W)];
+#pragma unroll
+      for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-G[t * (W + 1) + q], v, acc[q + 1]);
+      acc[W - 1] = fma(-G[t * (W + 1) + W - 1], v, enter);
+      tile[row(t) * TP] = v;
+    }
+  }
+}
+
+// Tiled variant: each warp stages TW lines in shared memory (coalesced loads/stores), and
 // every lane runs its substitution out of shared memory, so the sequential recurrence sees
-// shared-memory latency instead of DRAM latency.  Requires inner == 1 or inner % 32 == 0.
-template <int W, int WARPS, int TW>
+// shared-memory latency instead of DRAM latency.  With NBUF = 2 the warp streams: the
+// asynchronous loads of its next tile are in flight while the current tile is solved and
+// stored, so DRAM traffic overlaps the recurrences.  Requires inner == 1 or inner % 32 == 0
+// (lanes of a tile are consecutive lines).
+template <int W, int WARPS, int TW, int NBUF>
 __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restrict__ data, long long outer, int m,
-                                                               long long inner, const double* __restrict__ Lb,
-                                                               const double* __restrict__ inv, int mode,
-                                                               double omega, double* __restrict__ xacc) {
-  extern __shared__ double sh[];
-  double* sL = sh;                          // [m][W+1]
-  double* sI = sL + (size_t)m * (W + 1);    // [m]
+                                                               long long inner, const double* __restrict__ fac,
+                                                               int mode, double omega, double* __restrict__ xacc) {
+  extern __shared__ __align__(16) double sh[];
+  double* sF = sh;                          // [m][W+1]: forward column table (BandFactor::fac)
+  double* sB = sF + (size_t)m * (W + 1);    // [m][W+1]: backward column table
+  double* sI = sB + (size_t)m * (W + 1) + W;   // [-W, m+W): 1/L[k][k], zero outside [0, m)
   constexpr int TP = TW + 1;                // padded tile row (bank-conflict free for TW = 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* tile = sI + m + (size_t)warp * m * TP;   // [m][TP]
-  for (int i = threadIdx.x; i < m * (W + 1); i += blockDim.x) sL[i] = Lb[i];
-  for (int i = threadIdx.x; i < m; i += blockDim.x) sI[i] = inv[i];
+  const int MP = m + 2 * W;                 // tile rows incl. W zero rows on each side
+  double* tiles = sI + m + W + (size_t)warp * NBUF * MP * TP + W * TP;   // buffer b: tiles + b*MP*TP
+  // the factor (precomputed [sF | sB | sI], BandFactor::fac) arrives in one batch of async copies
+  const int flen = 2 * (W + 1) * m;
+  for (int i = threadIdx.x; i < flen; i += blockDim.x) ls_cp_async8(sh + i, fac + i);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) ls_cp_async8(sI + i, fac + flen + i);
+  for (int i = threadIdx.x; i < W; i += blockDim.x) sI[-1 - i] = sI[m + i] = 0.0;
+  for (int b = 0; b < NBUF; ++b) {
+    double* t = tiles + (size_t)b * MP * TP;
+    for (int i = lane; i < W * TP; i += 32) t[-W * TP + i] = t[m * TP + i] = 0.0;
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const long long lines = outer * inner;
   const long long groups = (lines + TW - 1) / TW;
-  for (long long g = (long long)blockIdx.x * WARPS + warp; g < groups; g += (long long)gridDim.x * WARPS) {
+  const long long stride = (long long)gridDim.x * WARPS;
+
+  auto issue_load = [&](long long g, double* tile) {
     const long long l0 = g * TW;
     const int nl = (int)min((long long)TW, lines - l0);
-    // ---- load the TW x m tile with asynchronous copies (all loads in flight at once)
     if (inner == 1) {
       const double* src = data + l0 * m;
-      for (int e = lane; e < nl * m; e += 32) ls_cp_async8(&tile[(e % m) * TP + e / m], src + e);
+      int k = lane % m, ln = lane / m;   // e = ln * m + k, advanced by 32 without divisions
+      for (int e = lane; e < nl * m; e += 32) {
+        ls_cp_async8(&tile[k * TP + ln], src + e);
+        k += 32;
+        while (k >= m) { k -= m; ++ln; }
+      }
     } else {   // lanes = consecutive lines: coalesced except where the group crosses an `outer` step
       const long long l = l0 + lane;
       const double* src = data + (l / inner) * (long long)m * inner + (l % inner);
+      double* tp = tile + lane;
       if (lane < nl)
-        for (int k = 0; k < m; ++k) ls_cp_async8(&tile[k * TP + lane], src + (long long)k * inner);
+#pragma unroll 4
+        for (int k = 0; k < m; ++k) {
+          ls_cp_async8(tp, src);
+          tp += TP;
+          src += inner;
+        }
     }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncwarp();
-    if (lane < nl) {
-      double win[W + 1];
-#pragma unroll
-      for (int j = 0; j <= W; ++j) win[j] = 0.0;
-      for (int k = 0; k < m; ++k) {
-#pragma unroll
-        for (int j = W; j >= 1; --j) win[j] = win[j - 1];
-        double acc = tile[k * TP + lane];
-        const double* Lr = sL + (size_t)k * (W + 1);
-#pragma unroll
-        for (int j = 1; j <= W; ++j) acc = fma(-Lr[W - j], win[j], acc);
-        win[0] = acc * sI[k];
-        tile[k * TP + lane] = win[0];
-      }
-#pragma unroll
-      for (int j = 0; j <= W; ++j) win[j] = 0.0;
-      for (int k = m - 1; k >= 0; --k) {
-#pragma unroll
-        for (int j = W; j >= 1; --j) win[j] = win[j - 1];
-        double acc = tile[k * TP + lane];
-#pragma unroll
-        for (int j = 1; j <= W; ++j)
-          if (k + j < m) acc = fma(-sL[(size_t)(k + j) * (W + 1) + W - j], win[j], acc);
-        win[0] = acc * sI[k];
-        tile[k * TP + lane] = win[0];
-      }
-    }
-    __syncwarp();
-    // ---- store (or accumulate omega * result into xacc, reading xacc 8 elements ahead so the
-    // read-modify-writes overlap instead of serialising on DRAM latency)
-    constexpr int U = 8;
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  // store (or accumulate omega * result into xacc, reading xacc U elements ahead so the
+  // read-modify-writes overlap instead of serialising on DRAM latency)
+  auto store = [&](long long g, const double* tile) {
+    const long long l0 = g * TW;
+    const int nl = (int)min((long long)TW, lines - l0);
+    constexpr int U = 16;
     if (inner == 1) {
       double* dst = (mode == 0 ? data : xacc) + l0 * m;
       const int tot = nl * m;
+      int k = lane % m, ln = lane / m;
       for (int e0 = lane; e0 < tot; e0 += 32 * U) {
         double xv[U];
         if (mode != 0) {
@@ -150,32 +231,71 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
         for (int u = 0; u < U; ++u) {
           const int e = e0 + 32 * u;
           if (e < tot) {
-            const double v = tile[(e % m) * TP + e / m];
+            const double v = tile[k * TP + ln];
             dst[e] = mode == 0 ? v : fma(omega, v, xv[u]);
+            k += 32;
+            while (k >= m) { k -= m; ++ln; }
           }
         }
       }
     } else {
       const long long l = l0 + lane;
       double* dst = (mode == 0 ? data : xacc) + (l / inner) * (long long)m * inner + (l % inner);
-      if (lane < nl)
-        for (int k0 = 0; k0 < m; k0 += U) {
-          double xv[U];
-          if (mode != 0) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = (k0 + u < m) ? dst[(long long)(k0 + u) * inner] : 0.0;
+      const double* tp = tile + lane;
+      if (lane < nl) {
+        if (mode == 0) {
+#pragma unroll 4
+          for (int k = 0; k < m; ++k) {
+            *dst = *tp;
+            tp += TP;
+            dst += inner;
           }
+        } else {
+          for (int k0 = 0; k0 < m; k0 += U) {
+            double xv[U];
+            const int nu = min(U, m - k0);
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int k = k0 + u;
-            if (k < m) {
-              const double v = tile[k * TP + lane];
-              dst[(long long)k * inner] = mode == 0 ? v : fma(omega, v, xv[u]);
-            }
+            for (int u = 0; u < U; ++u) xv[u] = u < nu ? dst[(long long)u * inner] : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (u < nu) dst[(long long)u * inner] = fma(omega, tp[u * TP], xv[u]);
+            tp += U * TP;
+            dst += (long long)U * inner;
           }
         }
+      }
+    }
+  };
+
+  long long g = (long long)blockIdx.x * WARPS + warp;
+  int cur = 0;
+  if (NBUF == 2 && g < groups) issue_load(g, tiles);
+  for (; g < groups; g += stride) {
+    double* tile = tiles + (size_t)cur * MP * TP;
+    if (NBUF == 2) {
+      const long long gn = g + stride;
+      if (gn < groups) {
+        issue_load(gn, tiles + (size_t)(cur ^ 1) * MP * TP);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // the current tile has landed
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+    } else {
+      issue_load(g, tile);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncwarp();
+    const int nl = (int)min((long long)TW, lines - g * TW);
+    if (lane < nl) {
+      // forward  y_k = i_k b_k - sum_j (i_k L[k][k-j]) y_{k-j}
+      // backward x_k = i_k y_k - sum_j (i_k L[k+j][k]) x_{k+j}
+      band_sweep<W, TP, true>(tile + lane, sF, sI, m);
+      band_sweep<W, TP, false>(tile + lane, sB, sI, m);
+    }
+    __syncwarp();
+    store(g, tile);
+    __syncwarp();
+    if (NBUF == 2) cur ^= 1;
   }
 }
 
@@ -207,41 +327,93 @@ void BandFactor::upload(const std::vector<double>& Lb_h, const std::vector<doubl
   IGACD_CUDA(cudaMalloc(&inv, sizeof(double) * inv_h.size()));
   IGACD_CUDA(cudaMemcpy(Lb, Lb_h.data(), sizeof(double) * Lb_h.size(), cudaMemcpyHostToDevice));
   IGACD_CUDA(cudaMemcpy(inv, inv_h.data(), sizeof(double) * inv_h.size(), cudaMemcpyHostToDevice));
+  // column-order tables for the tiled kernel: [Gf | Gb | I], rows of stride w+1 (see band_sweep)
+  //   Gf[t][q] = i_r L[r][t], r = t+1+q;   Gb[t][q] = i_r L[k][r], k = m-1-t, r = k-1-q
+  std::vector<double> f((size_t)(2 * (w + 1) + 1) * m, 0.0);
+  double* Gf = f.data();
+  double* Gb = Gf + (size_t)m * (w + 1);
+  double* Ih = Gb + (size_t)m * (w + 1);
+  auto Lh = [&](int i, int j) { return Lb_h[(size_t)i * (w + 1) + (w - (i - j))]; };   // j in [i-w, i]
+  for (int t = 0; t < m; ++t) {
+    Ih[t] = inv_h[t];
+    for (int q = 0; q < w; ++q) {
+      const int r = t + 1 + q;
+      if (r < m) Gf[(size_t)t * (w + 1) + q] = inv_h[r] * Lh(r, t);
+      const int k = m - 1 - t, rb = k - 1 - q;
+      if (rb >= 0) Gb[(size_t)t * (w + 1) + q] = inv_h[rb] * Lh(k, rb);
+    }
+  }
+  IGACD_CUDA(cudaMalloc(&fac, sizeof(double) * f.size()));
+  IGACD_CUDA(cudaMemcpy(fac, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice));
 }
 
 void BandFactor::release() {
   cudaFree(Lb);
   cudaFree(inv);
-  Lb = inv = nullptr;
+  cudaFree(fac);
+  Lb = inv = fac = nullptr;
 }
 
-template <int W, int WARPS, int TW>
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    IGACD_CUDA(cudaGetDevice(&dev));
+    IGACD_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int W, int WARPS, int TW, int NBUF>
 static bool try_tiled(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode,
                       double omega, double* xacc, cudaStream_t s) {
-  const size_t smem_t = sizeof(double) * ((size_t)m * (W + 1) + m + (size_t)WARPS * m * (TW + 1));
+  const size_t smem_t = sizeof(double) * (2 * (size_t)m * (W + 1) + m + 2 * W +
+                                          (size_t)WARPS * NBUF * (m + 2 * W) * (TW + 1));
   if (smem_t > 200 * 1024) return false;
   static size_t attr_t = 0;
   if (smem_t > 48 * 1024 && attr_t < smem_t) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_band_solve_tiled<W, WARPS, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem_t));
+    IGACD_CUDA(cudaFuncSetAttribute(k_band_solve_tiled<W, WARPS, TW, NBUF>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
     attr_t = smem_t;
   }
   const long long groups = (outer * inner + TW - 1) / TW;
   long long blocks = (groups + WARPS - 1) / WARPS;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  k_band_solve_tiled<W, WARPS, TW><<<(unsigned)blocks, 32 * WARPS, smem_t, s>>>(data, outer, m, inner, F.Lb, F.inv,
-                                                                              mode, omega, xacc);
+  // persistent grid: the factor is staged once per resident block, not once per tile
+  static size_t occ_smem = 0;
+  static int occ = 1;
+  if (occ_smem != smem_t) {
+    IGACD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_band_solve_tiled<W, WARPS, TW, NBUF>,
+                                                             32 * WARPS, smem_t));
+    occ = std::max(occ, 1);
+    occ_smem = smem_t;
+  }
+  blocks = std::min<long long>(blocks, (long long)occ * num_sms());
+  k_band_solve_tiled<W, WARPS, TW, NBUF><<<(unsigned)blocks, 32 * WARPS, smem_t, s>>>(data, outer, m, inner, F.fac,
+                                                                                    mode, omega, xacc);
   return true;
+}
+
+// IGACD_BAND_NBUF=2 selects the double-buffered line-solve pipeline (2 warps per SM); in round 1
+// it measured no faster than single-buffered tiles at 4 warps per SM (config 4: 42 vs 40 us).
+static int band_nbuf() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IGACD_BAND_NBUF");
+    v = (e && e[0] == '2') ? 2 : 1;
+  }
+  return v;
 }
 
 template <int W>
 static void launch_w(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode,
                      double omega, double* xacc, cudaStream_t s) {
-  // widest tile that fits: 32 lines per warp (2 warps), else 16 or 8 lines (1 warp)
-  if (try_tiled<W, 2, 32>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
-  if (try_tiled<W, 1, 32>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
-  if (try_tiled<W, 1, 16>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
-  if (try_tiled<W, 1, 8>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  // double-buffered 32-line tiles (2 warps) when they fit, else the widest single-buffered tile
+  if (band_nbuf() == 2 && try_tiled<W, 2, 32, 2>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  if (try_tiled<W, 2, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  if (try_tiled<W, 1, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  if (try_tiled<W, 1, 16, 1>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  if (try_tiled<W, 1, 8, 1>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
   const size_t smem = sizeof(double) * ((size_t)m * (W + 1) + m);
   static int attr_set = 0;
   if (smem > 48 * 1024 && attr_set < (int)smem) {

@@ -26,23 +26,29 @@ __global__ void k_axis_pass_fast(const double* __restrict__ in, double* __restri
   }
 }
 
-// inner > 1: blockIdx.y = output row (ou, o), threads along the contiguous inner index
+// inner > 1: blockIdx.y = a group of RB consecutive output rows (ou, o), threads along the
+// contiguous inner index.  One thread produces the RB outputs of its column, so the input rows
+// those outputs share (P has overlapping row windows) are re-read from L1, not from L2.
+constexpr int RB = 8;
 __global__ void k_axis_pass_rows(const double* __restrict__ in, double* __restrict__ out, int rows, int nin, int nout,
                                  int inner, const int* __restrict__ start, const double* __restrict__ w, int W,
                                  int accumulate) {
-  const int row = blockIdx.y + blockIdx.z * gridDim.y;
-  if (row >= rows) return;
-  const int o = row % nout, ou = row / nout;
-  const int st = __ldg(start + o);
-  const double* wr = w + o * W;
-  const double* src = in + ((long long)ou * nin + st) * inner;
-  double* dst = out + (long long)row * inner;
+  const int row0 = (blockIdx.y + blockIdx.z * gridDim.y) * RB;
+  if (row0 >= rows) return;
+  const int row1 = min(row0 + RB, rows);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < inner; i += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int k = 0; k < W; ++k)
-      if (st + k < nin) acc = fma(__ldg(wr + k), __ldg(src + (long long)k * inner + i), acc);
-    if (accumulate) dst[i] += acc;
-    else dst[i] = acc;
+    for (int row = row0; row < row1; ++row) {
+      const int o = row % nout, ou = row / nout;
+      const int st = __ldg(start + o);
+      const double* wr = w + o * W;
+      const double* src = in + ((long long)ou * nin + st) * inner + i;
+      double acc = 0.0;
+      for (int k = 0; k < W; ++k)
+        if (st + k < nin) acc = fma(__ldg(wr + k), __ldg(src + (long long)k * inner), acc);
+      double* dst = out + (long long)row * inner + i;
+      if (accumulate) *dst += acc;
+      else *dst = acc;
+    }
   }
 }
 
@@ -57,8 +63,9 @@ static void axis_pass(Handle& h, const double* in, double* out, long long outer,
                                                                     acc ? 1 : 0);
   } else {
     const long long rows = outer * nout;
-    const int gy = (int)std::min(rows, 65535LL);
-    const int gz = (int)((rows + gy - 1) / gy);
+    const long long groups = (rows + RB - 1) / RB;
+    const int gy = (int)std::min(groups, 65535LL);
+    const int gz = (int)((groups + gy - 1) / gy);
     const int gx = (int)std::min((inner + bs - 1) / bs, 65535LL);
     k_axis_pass_rows<<<dim3(gx, gy, gz), bs, 0, s>>>(in, out, (int)rows, nin, nout, (int)inner, start, w, W,
                                                      acc ? 1 : 0);
