@@ -249,6 +249,19 @@ void build_transfer(Handle& h, int p, int nc, Transfer1D& T, cudaStream_t s) {
   }
   T.wp = wp;
   T.wr = wr;
+  // widest input window of a tile of TO consecutive output rows (transfer.cu k_transfer2d)
+  auto window = [](const std::vector<int>& st, int W, int nin, int TO) {
+    int best = 1;
+    for (size_t a = 0; a < st.size(); a += 1) {
+      const size_t b = std::min(st.size(), a + TO) - 1;
+      best = std::max(best, std::min(st[b] + W, nin) - st[a]);
+    }
+    return best;
+  };
+  T.pwin1 = window(ps, wp, mc, TRANSFER_TO1);
+  T.pwin2 = window(ps, wp, mc, TRANSFER_TO2);
+  T.rwin1 = window(rs, wr, mf, TRANSFER_TO1);
+  T.rwin2 = window(rs, wr, mf, TRANSFER_TO2);
   IGACD_CUDA(cudaMalloc(&T.p_start, sizeof(int) * mf));
   IGACD_CUDA(cudaMalloc(&T.p_w, sizeof(double) * pw.size()));
   IGACD_CUDA(cudaMalloc(&T.r_start, sizeof(int) * mc));

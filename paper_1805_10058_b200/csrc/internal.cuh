@@ -56,7 +56,10 @@ struct Transfer1D {   // 1D prolongation P (m_f x m_c) in fixed-width row storag
   int* r_start = nullptr;       // [mc]  first fine column of coarse row c (row of P^T)
   double* r_w = nullptr;        // [mc][wr]
   std::vector<double> hdense;   // host dense copy (debug/parity)
+  // input-window sizes of a TRANSFER_TO1 (TO2) output tile, for P (p*) and P^T (r*)
+  int pwin1 = 0, pwin2 = 0, rwin1 = 0, rwin2 = 0;
 };
+constexpr int TRANSFER_TO1 = 16, TRANSFER_TO2 = 32;   // k_transfer2d output tile
 
 // Banded Cholesky factor F = L L^T on the device (linesolve.cu).
 struct BandFactor {

@@ -74,18 +74,93 @@ static void axis_pass(Handle& h, const double* in, double* out, long long outer,
   count_launch(h);
 }
 
+
+// Both fastest axes in one pass (2D: the whole transfer; 3D: the in-slab part):
+//   out[o1][o2] (+)= sum_{k1,k2} T[o1][k1] T[o2][k2] in[st(o1)+k1][st(o2)+k2]
+// for every [nin][nin] slab of `in` (blockIdx.z = slab).  A CTA owns a TO1 x TO2 output tile:
+// the input window it needs is staged in shared memory (coalesced rows), contracted along
+// axis 2 into a [rows][TO2] intermediate, then along axis 1, so each input element is read
+// from DRAM once (window halos come from L2) instead of once per 1D pass.
+constexpr int TO1 = TRANSFER_TO1, TO2 = TRANSFER_TO2, NT2 = 256;
+
+__global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ in, double* __restrict__ out, int nin,
+                                                    int nout, const int* __restrict__ start,
+                                                    const double* __restrict__ w, int W, int accumulate) {
+  extern __shared__ __align__(16) double sm2[];
+  const int o1a = blockIdx.y * TO1, o2a = blockIdx.x * TO2;
+  const int o1b = min(o1a + TO1, nout), o2b = min(o2a + TO2, nout);
+  const int i1a = __ldg(start + o1a), i2a = __ldg(start + o2a);
+  const int i1b = min(__ldg(start + o1b - 1) + W, nin), i2b = min(__ldg(start + o2b - 1) + W, nin);
+  const int IR = i1b - i1a, IC = i2b - i2a;
+  const int ICP = IC | 1;   // odd row pitch: conflict-free column walks
+  double* xin = sm2;                       // [IR][ICP]
+  double* tmp = sm2 + IR * ICP;            // [IR][TO2]
+  const double* src = in + (size_t)blockIdx.z * nin * nin;
+  for (int e = threadIdx.x; e < IR * IC; e += NT2) {
+    const int r = e / IC, c = e - r * IC;
+    xin[r * ICP + c] = __ldg(src + (size_t)(i1a + r) * nin + i2a + c);
+  }
+  __syncthreads();
+  // axis 2: tmp[r][c2] = sum_k T[o2][k] xin[r][st(o2) - i2a + k]
+  const int nc2 = o2b - o2a;
+  for (int e = threadIdx.x; e < IR * TO2; e += NT2) {
+    const int r = e / TO2, c2 = e - r * TO2;
+    double acc = 0.0;
+    if (c2 < nc2) {
+      const int o2 = o2a + c2;
+      const int st = __ldg(start + o2);
+      const int kn = min(W, nin - st);
+      const double* wr = w + (size_t)o2 * W;
+      const double* xr = xin + r * ICP + (st - i2a);
+      for (int k = 0; k < kn; ++k) acc = fma(__ldg(wr + k), xr[k], acc);
+    }
+    tmp[r * TO2 + c2] = acc;
+  }
+  __syncthreads();
+  // axis 1: out[o1][o2] = sum_k T[o1][k] tmp[st(o1) - i1a + k][c2]
+  double* dst = out + (size_t)blockIdx.z * nout * nout;
+  for (int e = threadIdx.x; e < TO1 * TO2; e += NT2) {
+    const int r1 = e / TO2, c2 = e - r1 * TO2;
+    const int o1 = o1a + r1;
+    if (o1 >= o1b || c2 >= nc2) continue;
+    const int st = __ldg(start + o1);
+    const int kn = min(W, nin - st);
+    const double* wr = w + (size_t)o1 * W;
+    const double* tr = tmp + (st - i1a) * TO2 + c2;
+    double acc = 0.0;
+    for (int k = 0; k < kn; ++k) acc = fma(__ldg(wr + k), tr[k * TO2], acc);
+    double* d = dst + (size_t)o1 * nout + o2a + c2;
+    if (accumulate) *d += acc;
+    else *d = acc;
+  }
+}
+
+// win1/win2: widest input window of a TO1-row / TO2-column output tile (Transfer1D)
+static void transfer2d(Handle& h, const double* in, double* out, long long slabs, int nin, int nout, const int* start,
+                       const double* w, int W, int win1, int win2, bool acc, cudaStream_t s) {
+  const size_t smem = sizeof(double) * ((size_t)win1 * (win2 | 1) + (size_t)win1 * TO2);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    IGACD_CUDA(cudaFuncSetAttribute(k_transfer2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const dim3 grid((nout + TO2 - 1) / TO2, (nout + TO1 - 1) / TO1, (unsigned)slabs);
+  k_transfer2d<<<grid, NT2, smem, s>>>(in, out, nin, nout, start, w, W, acc ? 1 : 0);
+  IGACD_LAUNCH_CHECK();
+  count_launch(h);
+}
+
 // level l (fine, m_f) <- level l+1 (coarse, m_c)
 void launch_prolong(Handle& h, int nc, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s) {
   const Transfer1D& T = h.tr[level];
   const long long d = nc, mf = T.mf, mc = T.mc;
   if (h.dim == 2) {
-    // [d][mc][mc] -> [d][mc][mf] -> [d][mf][mf]
-    axis_pass(h, xc, h.scratch0, d * mc, (int)mc, (int)mf, 1, T.p_start, T.p_w, T.wp, false, s);
-    axis_pass(h, h.scratch0, xf, d, (int)mc, (int)mf, mf, T.p_start, T.p_w, T.wp, accumulate, s);
+    // [d][mc][mc] -> [d][mf][mf] in one pass
+    transfer2d(h, xc, xf, d, (int)mc, (int)mf, T.p_start, T.p_w, T.wp, T.pwin1, T.pwin2, accumulate, s);
   } else {
-    axis_pass(h, xc, h.scratch0, d * mc * mc, (int)mc, (int)mf, 1, T.p_start, T.p_w, T.wp, false, s);
-    axis_pass(h, h.scratch0, h.scratch1, d * mc, (int)mc, (int)mf, mf, T.p_start, T.p_w, T.wp, false, s);
-    axis_pass(h, h.scratch1, xf, d, (int)mc, (int)mf, mf * mf, T.p_start, T.p_w, T.wp, accumulate, s);
+    // axis 0: [d][mc][mc][mc] -> [d][mf][mc][mc]; axes 1, 2 per slab: -> [d][mf][mf][mf]
+    axis_pass(h, xc, h.scratch0, d, (int)mc, (int)mf, mc * mc, T.p_start, T.p_w, T.wp, false, s);
+    transfer2d(h, h.scratch0, xf, d * mf, (int)mc, (int)mf, T.p_start, T.p_w, T.wp, T.pwin1, T.pwin2, accumulate, s);
   }
 }
 
@@ -93,13 +168,11 @@ void launch_restrict(Handle& h, int nc, int level, const double* xf, double* xc,
   const Transfer1D& T = h.tr[level];
   const long long d = nc, mf = T.mf, mc = T.mc;
   if (h.dim == 2) {
-    // [d][mf][mf] -> [d][mc][mf] -> [d][mc][mc]
-    axis_pass(h, xf, h.scratch0, d, (int)mf, (int)mc, mf, T.r_start, T.r_w, T.wr, false, s);
-    axis_pass(h, h.scratch0, xc, d * mc, (int)mf, (int)mc, 1, T.r_start, T.r_w, T.wr, false, s);
+    transfer2d(h, xf, xc, d, (int)mf, (int)mc, T.r_start, T.r_w, T.wr, T.rwin1, T.rwin2, false, s);
   } else {
-    axis_pass(h, xf, h.scratch0, d, (int)mf, (int)mc, mf * mf, T.r_start, T.r_w, T.wr, false, s);
-    axis_pass(h, h.scratch0, h.scratch1, d * mc, (int)mf, (int)mc, mf, T.r_start, T.r_w, T.wr, false, s);
-    axis_pass(h, h.scratch1, xc, d * mc * mc, (int)mf, (int)mc, 1, T.r_start, T.r_w, T.wr, false, s);
+    // axes 1, 2 per fine slab: [d][mf][mf][mf] -> [d][mf][mc][mc]; axis 0: -> [d][mc][mc][mc]
+    transfer2d(h, xf, h.scratch0, d * mf, (int)mf, (int)mc, T.r_start, T.r_w, T.wr, T.rwin1, T.rwin2, false, s);
+    axis_pass(h, h.scratch0, xc, d, (int)mf, (int)mc, mc * mc, T.r_start, T.r_w, T.wr, false, s);
   }
 }
 
