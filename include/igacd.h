@@ -97,6 +97,7 @@ int igacd_vcycle(igacd_handle h, const double* b, double* x, void* stream);
  * Pi s = b0 s, Vs = V-cycle of the scalar operator A_s = Pi^T A Pi on the same levels. */
 #define IGACD_PRECOND_VCYCLE 0
 #define IGACD_PRECOND_AUX 1
+#define IGACD_PRECOND_AUX_ADD 2
 int igacd_precond(igacd_handle h, const double* b, double* x, void* stream);
 int igacd_set_preconditioner(igacd_handle h, int mode);
 int igacd_get_preconditioner(igacd_handle h, int* mode);
@@ -124,6 +125,18 @@ int igacd_aux_omega(igacd_handle h, int level, double* omega, double* rho);
  * iters, relres: host outputs (may be NULL).  Synchronises `stream`.
  * Returns IGACD_E_NOCONV (x still written) when maxit is reached. */
 int igacd_solve(igacd_handle h, const double* b, double* x, double tol, int maxit, int* iters,
+                double* relres, void* stream);
+
+/* Flexible right-preconditioned restarted GMRES -- the paper's PGMRES (PAPER.md:1075, 1260:
+ * "a preconditioned generalized minimal residual (PGMRES) method").  Same preconditioner as
+ * igacd_solve (igacd_set_preconditioner), zero initial guess, Arnoldi by classical
+ * Gram-Schmidt with one re-orthogonalisation (CGS2), Givens rotations on the host; stop when
+ * the Arnoldi residual estimate |g_{k+1}| / ||r_0||_2 < tol or after maxit products A z.
+ * restart in [1, 512]: the Krylov basis V (restart+1 vectors) and Z = B V (restart vectors)
+ * of level-0 size are allocated on the device on first use and owned by the handle.
+ * iters, relres: host outputs (may be NULL).  Synchronises `stream` once per iteration.
+ * Returns IGACD_E_NOCONV (x still written) when maxit is reached. */
+int igacd_gmres(igacd_handle h, const double* b, double* x, double tol, int maxit, int restart, int* iters,
                 double* relres, void* stream);
 
 /* As igacd_solve with HOST b and x (pinned or pageable); the host<->device copies are

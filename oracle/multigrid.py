@@ -147,12 +147,16 @@ def aux_map(d: int, nscal: int, b0) -> sp.csr_matrix:
 
 
 class AuxPreconditioner:
-    """Reading R8: z = Pi Bs Pi^T r;  z += V (r - A z);  z += Pi Bs Pi^T (r - A z).
+    """Reading R8: z = Pi Bs Pi^T r;  z += V (r - A z);  z += Pi Bs Pi^T (r - A z)
+    (mode "mult", symmetric multiplicative), or mode "add": z = V r + Pi Bs Pi^T r
+    (additive subspace correction, reading R8').
 
     Bs = exact A_s^{-1} (sparse LU, library primitive) when b0 has exactly one nonzero
     component (A_s is then one Kronecker product), else the V-cycle of A_s."""
 
-    def __init__(self, A0, d, p, n, b0, levels=0, nu_pre=1, nu_post=1, smoother="toeplitz"):
+    def __init__(self, A0, d, p, n, b0, levels=0, nu_pre=1, nu_post=1, smoother="toeplitz", mode="mult"):
+        assert mode in ("mult", "add")
+        self.mode = mode
         self.A = sp.csr_matrix(A0)
         self.V = Hierarchy(A0, d, p, n, levels, nu_pre, nu_post, smoother=smoother)
         self.Pi = aux_map(d, A0.shape[0] // d, b0)
@@ -166,6 +170,8 @@ class AuxPreconditioner:
             self.Bs = self.Vs.vcycle
 
     def __call__(self, r):
+        if self.mode == "add":
+            return self.V.vcycle(r) + self.Pi @ self.Bs(self.Pi.T @ r)
         z = self.Pi @ self.Bs(self.Pi.T @ r)
         z = z + self.V.vcycle(r - self.A @ z)
         z = z + self.Pi @ self.Bs(self.Pi.T @ (r - self.A @ z))

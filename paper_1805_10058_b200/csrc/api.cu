@@ -122,6 +122,8 @@ static void destroy_handle(Handle* h) {
   cudaFree(h->scal);
   if (h->hscal) cudaFreeHost(h->hscal);
   for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar, h->zbuf}) cudaFree(v);
+  for (double* v : {h->gm_v, h->gm_z, h->gm_partial, h->gm_dev}) cudaFree(v);
+  if (h->gm_host) cudaFreeHost(h->gm_host);
   for (auto& pr : h->ev_pending) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
@@ -425,6 +427,13 @@ static void precond_apply(Handle& h, const double* r, double* z, cudaStream_t s)
   SysLevel& a0 = A.lv[0];
   Epi ep{};
   ep.b = r;
+  if (h.precond == PRECOND_AUX_ADD) {   // additive: z = V r + Pi B_s Pi^T r
+    vcycle_level(h, 0, 0, r, z, s);
+    launch_pi_t(h, r, a0.b, s);
+    aux_solve(h, a0.b, a0.x, s);
+    launch_pi(h, a0.x, z, true, s);
+    return;
+  }
   launch_pi_t(h, r, a0.b, s);
   aux_solve(h, a0.b, a0.x, s);
   launch_pi(h, a0.x, z, false, s);
@@ -497,6 +506,122 @@ static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int
     h.ev_pending.clear();
   }
   if (iters) *iters = std::min(it, maxit);
+  if (relres) *relres = rel;
+  return rel < tol ? IGACD_OK : IGACD_E_NOCONV;
+}
+
+
+// ---- FGMRES ------------------------------------------------------------------------------
+// Flexible right-preconditioned GMRES(restart) (the paper's PGMRES; oracle
+// krylov.fgmres): z_j = B v_j (precond_apply), w = A z_j, CGS2 Arnoldi with fused multi-dot
+// and multi-axpy kernels (coefficients stay on the device), Givens rotations of the small
+// Hessenberg matrix on the host (one device->host copy per step, as PCG's residual check),
+// x = Z y at convergence / restart; a restart recomputes the true residual b - A x.
+static void gm_workspace(Handle& h, int restart) {
+  if (h.gm_restart >= restart) return;
+  for (double* v : {h.gm_v, h.gm_z, h.gm_partial, h.gm_dev}) cudaFree(v);
+  if (h.gm_host) cudaFreeHost(h.gm_host);
+  h.gm_v = h.gm_z = h.gm_partial = h.gm_dev = h.gm_host = nullptr;
+  h.gm_restart = 0;
+  const size_t N = h.sys[0].lv[0].ndof;
+  IGACD_CUDA(cudaMalloc(&h.gm_v, sizeof(double) * N * (restart + 1)));
+  IGACD_CUDA(cudaMalloc(&h.gm_z, sizeof(double) * N * restart));
+  IGACD_CUDA(cudaMalloc(&h.gm_partial, sizeof(double) * MDOT * vec_ctas(N)));
+  const size_t nd = 3 * (size_t)restart + 3;
+  IGACD_CUDA(cudaMalloc(&h.gm_dev, sizeof(double) * nd));
+  IGACD_CUDA(cudaMallocHost(&h.gm_host, sizeof(double) * nd));
+  h.gm_restart = restart;
+}
+
+static int fgmres(Handle& h, const double* b, double* x, double tol, int maxit, int restart, int* iters,
+                  double* relres, cudaStream_t s) {
+  const size_t N = h.sys[0].lv[0].ndof;
+  gm_workspace(h, restart);
+  std::vector<const double*> V(restart + 1), Z(restart);
+  for (int j = 0; j <= restart; ++j) V[j] = h.gm_v + (size_t)j * N;
+  for (int j = 0; j < restart; ++j) Z[j] = h.gm_z + (size_t)j * N;
+  double* dh1 = h.gm_dev;                  // [restart + 1]
+  double* dh2 = dh1 + restart + 1;         // [restart + 1]
+  double* dsq = dh2 + restart + 1;         // [1]
+  double* dy = dsq + 1;                    // [restart]
+  double* hh = h.gm_host;
+  const int nv = vec_ctas(N);
+  double* v0 = h.gm_v;
+  launch_copy(h, b, v0, N, s);
+  launch_zero(h, x, N, s);
+  launch_dot(h, v0, v0, N, h.partial, s);
+  const double r0 = std::sqrt(reduce_to_host(h, nv, S_RR, s));
+  if (iters) *iters = 0;
+  if (relres) *relres = 0.0;
+  if (r0 == 0.0) return IGACD_OK;
+  double beta = r0, rel = 1.0;
+  int it = 0;
+  std::vector<double> H((size_t)(restart + 1) * restart), g(restart + 1), cs(restart), sn(restart), y(restart);
+  auto Hm = [&](int i, int j) -> double& { return H[(size_t)i * restart + j]; };
+  Epi ep{};
+  for (;;) {
+    launch_scal(h, v0, 1.0 / beta, N, s);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int k = 0;
+    bool done = false;
+    for (int j = 0; j < restart; ++j) {
+      double* zj = h.gm_z + (size_t)j * N;
+      double* w = h.gm_v + (size_t)(j + 1) * N;
+      precond_apply(h, V[j], zj, s);
+      launch_operator(h, 0, 0, zj, w, EPI_APPLY, DOT_NONE, ep, s);
+      ++it;
+      launch_mdot(h, w, V.data(), j + 1, N, h.gm_partial, dh1, s);   // CGS2, pass 1
+      launch_maxpy(h, w, V.data(), j + 1, dh1, -1.0, N, s);
+      launch_mdot(h, w, V.data(), j + 1, N, h.gm_partial, dh2, s);   // pass 2
+      launch_maxpy(h, w, V.data(), j + 1, dh2, -1.0, N, s);
+      launch_dot(h, w, w, N, h.partial, s);
+      launch_finalize(h, h.partial, nv, dsq, s);
+      IGACD_CUDA(cudaMemcpyAsync(hh, h.gm_dev, sizeof(double) * (2 * (restart + 1) + 1), cudaMemcpyDeviceToHost, s));
+      IGACD_CUDA(cudaStreamSynchronize(s));
+      const double hn = std::sqrt(hh[2 * (restart + 1)]);
+      for (int i = 0; i <= j; ++i) Hm(i, j) = hh[i] + hh[restart + 1 + i];
+      if (j + 1 <= restart) Hm(j + 1, j) = hn;
+      for (int i = 0; i < j; ++i) {   // previous rotations
+        const double a = Hm(i, j), c = Hm(i + 1, j);
+        Hm(i, j) = cs[i] * a + sn[i] * c;
+        Hm(i + 1, j) = -sn[i] * a + cs[i] * c;
+      }
+      const double den = std::hypot(Hm(j, j), Hm(j + 1, j));
+      cs[j] = Hm(j, j) / den;
+      sn[j] = Hm(j + 1, j) / den;
+      Hm(j, j) = den;
+      Hm(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      rel = std::fabs(g[j + 1]) / r0;
+      k = j + 1;
+      if (rel < tol || it >= maxit || hn == 0.0) {
+        done = true;
+        break;
+      }
+      launch_scal(h, w, 1.0 / hn, N, s);
+    }
+    for (int i = k - 1; i >= 0; --i) {   // back substitution H[:k,:k] y = g[:k]
+      double acc = g[i];
+      for (int l = i + 1; l < k; ++l) acc -= Hm(i, l) * y[l];
+      y[i] = acc / Hm(i, i);
+    }
+    IGACD_CUDA(cudaMemcpyAsync(dy, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
+    launch_maxpy(h, x, Z.data(), k, dy, 1.0, N, s);
+    IGACD_CUDA(cudaStreamSynchronize(s));   // y (pageable) is reused by the next cycle
+    if (done) break;
+    Epi er{};
+    er.b = b;
+    launch_operator(h, 0, 0, x, v0, EPI_RESID, DOT_NONE, er, s);
+    launch_dot(h, v0, v0, N, h.partial, s);
+    beta = std::sqrt(reduce_to_host(h, nv, S_RR, s));
+    if (beta == 0.0) {
+      rel = 0.0;
+      break;
+    }
+  }
+  if (iters) *iters = it;
   if (relres) *relres = rel;
   return rel < tol ? IGACD_OK : IGACD_E_NOCONV;
 }
@@ -697,8 +822,9 @@ int igacd_precond(igacd_handle h, const double* b, double* x, void* stream) {
 int igacd_set_preconditioner(igacd_handle h, int mode) {
   API_BEGIN
   Handle* hh = H(h);
-  if (mode != PRECOND_VCYCLE && mode != PRECOND_AUX) throw Error{IGACD_E_ARG, "unknown preconditioner"};
-  if (mode == PRECOND_AUX && !hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space (b0 = 0 or lambda = 0)"};
+  if (mode != PRECOND_VCYCLE && mode != PRECOND_AUX && mode != PRECOND_AUX_ADD)
+    throw Error{IGACD_E_ARG, "unknown preconditioner"};
+  if (mode != PRECOND_VCYCLE && !hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space (b0 = 0 or lambda = 0)"};
   hh->precond = mode;
   API_END
 }
@@ -767,6 +893,24 @@ int igacd_solve(igacd_handle h, const double* b, double* x, double tol, int maxi
   const int rc = pcg(*hh, b, x, tol, maxit, iters, relres, (cudaStream_t)stream);
   if (rc != IGACD_OK) {
     set_error("PCG reached maxit without the requested relative residual");
+    return rc;
+  }
+  API_END
+}
+
+
+int igacd_gmres(igacd_handle h, const double* b, double* x, double tol, int maxit, int restart, int* iters,
+                double* relres, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_ptr(b);
+  check_ptr(x);
+  if (b == x) throw Error{IGACD_E_ARG, "b and x must not alias"};
+  if (!(tol > 0) || maxit < 1) throw Error{IGACD_E_ARG, "need tol > 0 and maxit >= 1"};
+  if (restart < 1 || restart > 512) throw Error{IGACD_E_ARG, "restart must be in [1, 512]"};
+  const int rc = fgmres(*hh, b, x, tol, maxit, restart, iters, relres, (cudaStream_t)stream);
+  if (rc != IGACD_OK) {
+    set_error("GMRES reached maxit without the requested relative residual");
     return rc;
   }
   API_END

@@ -108,7 +108,7 @@ struct System {
   BandFactor tf[3];
 };
 
-enum Precond { PRECOND_VCYCLE = 0, PRECOND_AUX = 1 };
+enum Precond { PRECOND_VCYCLE = 0, PRECOND_AUX = 1, PRECOND_AUX_ADD = 2 };
 
 struct Handle {
   int dim = 0, p = 0;
@@ -132,6 +132,13 @@ struct Handle {
   double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *px = nullptr, *pb = nullptr;
   double *aw = nullptr, *ar = nullptr;   // aux preconditioner work (level-0 vector size)
   double* zbuf = nullptr;                // 3D split operator: 3*nc per-point combinations (level-0 size)
+  // FGMRES workspace (allocated on first use): Arnoldi basis V [restart+1][N], Z [restart][N]
+  int gm_restart = 0;
+  double* gm_v = nullptr;
+  double* gm_z = nullptr;
+  double* gm_partial = nullptr;   // MDOT * vec_ctas(N)
+  double* gm_dev = nullptr;       // [h1 (r+1) | h2 (r+1) | ||w||^2 | y (r)]
+  double* gm_host = nullptr;      // pinned mirror
   cudaStream_t stream = nullptr;
   // instrumentation
   long long launches = 0, apply_launches = 0;
@@ -196,6 +203,14 @@ void launch_pcg_update_xr(Handle& h, double* x, double* r, const double* p, cons
                           const double* rz, const double* pq, double* partial, cudaStream_t s);
 void launch_pcg_update_p(Handle& h, double* p, const double* z, size_t n, const double* rz_new,
                          const double* rz_old, cudaStream_t s);
+// GMRES (Arnoldi): dst[j] = (w, V[j]) for j < nv (partial: MDOT * vec_ctas(n) doubles);
+// w += sign * sum_j c[j] V[j] (c on the device);  a *= f
+constexpr int MDOT = 8;
+void launch_mdot(Handle& h, const double* w, const double* const* V, int nv, size_t n, double* partial, double* dst,
+                 cudaStream_t s);
+void launch_maxpy(Handle& h, double* w, const double* const* V, int nv, const double* c, double sign, size_t n,
+                  cudaStream_t s);
+void launch_scal(Handle& h, double* a, double f, size_t n, cudaStream_t s);
 
 // ---- linesolve.cu -------------------------------------------------------------------
 void band_cholesky(const std::vector<double>& F, int m, int w, std::vector<double>& Lb, std::vector<double>& inv);

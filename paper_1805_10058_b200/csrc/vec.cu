@@ -2,6 +2,8 @@
 // Dot products: each CTA of a fixed-size grid reduces its grid-stride share (warp shuffle,
 // then shared memory) into partial[blockIdx.x]; a one-CTA finalize sums the partials in a
 // fixed order.  Scalars (alpha, beta numerators/denominators) stay on the device.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace igacd {
@@ -186,6 +188,91 @@ void launch_pcg_update_xr(Handle& h, double* x, double* r, const double* p, cons
 void launch_pcg_update_p(Handle& h, double* p, const double* z, size_t n, const double* rzn, const double* rzo,
                          cudaStream_t s) {
   k_pcg_p<<<vec_ctas(n), VBS, 0, s>>>(p, z, n, rzn, rzo);
+  LAUNCH_TAIL();
+}
+
+
+// ---- GMRES (Arnoldi) kernels: up to MDOT vectors per launch -----------------------------------
+struct VecSet {
+  const double* v[MDOT];
+};
+
+// partial[j * np + cta] = sum_i w_i v_j,i  (j < nv), fixed-order block reductions
+__global__ void k_mdot(const double* __restrict__ w, VecSet V, int nv, size_t n, double* partial, int np) {
+  __shared__ double red[VBS / 32];
+  double s[MDOT];
+#pragma unroll
+  for (int j = 0; j < MDOT; ++j) s[j] = 0.0;
+  for (size_t i = blockIdx.x * (size_t)VBS + threadIdx.x; i < n; i += (size_t)gridDim.x * VBS) {
+    const double wi = w[i];
+#pragma unroll
+    for (int j = 0; j < MDOT; ++j)
+      if (j < nv) s[j] = fma(wi, V.v[j][i], s[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < MDOT; ++j) {
+    if (j >= nv) break;
+    const double t = block_sum(s[j], red);
+    if (threadIdx.x == 0) partial[j * np + blockIdx.x] = t;
+    __syncthreads();
+  }
+}
+
+// dst[j] = sum_c partial[j * np + c], one block per j
+__global__ void k_finalize_multi(const double* partial, int np, double* dst) {
+  __shared__ double red[VBS / 32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += VBS) s += partial[blockIdx.x * np + i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) dst[blockIdx.x] = s;
+}
+
+// w += sign * sum_j c_j v_j  (c on the device)
+__global__ void k_maxpy(double* __restrict__ w, VecSet V, int nv, const double* __restrict__ c, double sign,
+                        size_t n) {
+  double cj[MDOT];
+#pragma unroll
+  for (int j = 0; j < MDOT; ++j) cj[j] = j < nv ? sign * c[j] : 0.0;
+  for (size_t i = blockIdx.x * (size_t)VBS + threadIdx.x; i < n; i += (size_t)gridDim.x * VBS) {
+    double a = w[i];
+#pragma unroll
+    for (int j = 0; j < MDOT; ++j)
+      if (j < nv) a = fma(cj[j], V.v[j][i], a);
+    w[i] = a;
+  }
+}
+
+__global__ void k_scal(double* a, double f, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)VBS + threadIdx.x; i < n; i += (size_t)gridDim.x * VBS) a[i] *= f;
+}
+
+void launch_mdot(Handle& h, const double* w, const double* const* V, int nv, size_t n, double* partial, double* dst,
+                 cudaStream_t s) {
+  const int np = vec_ctas(n);
+  for (int g = 0; g < nv; g += MDOT) {
+    VecSet vs{};
+    const int k = std::min(MDOT, nv - g);
+    for (int j = 0; j < k; ++j) vs.v[j] = V[g + j];
+    k_mdot<<<np, VBS, 0, s>>>(w, vs, k, n, partial, np);
+    LAUNCH_TAIL();
+    k_finalize_multi<<<k, VBS, 0, s>>>(partial, np, dst + g);
+    LAUNCH_TAIL();
+  }
+}
+
+void launch_maxpy(Handle& h, double* w, const double* const* V, int nv, const double* c, double sign, size_t n,
+                  cudaStream_t s) {
+  for (int g = 0; g < nv; g += MDOT) {
+    VecSet vs{};
+    const int k = std::min(MDOT, nv - g);
+    for (int j = 0; j < k; ++j) vs.v[j] = V[g + j];
+    k_maxpy<<<vec_ctas(n), VBS, 0, s>>>(w, vs, k, c + g, sign, n);
+    LAUNCH_TAIL();
+  }
+}
+
+void launch_scal(Handle& h, double* a, double f, size_t n, cudaStream_t s) {
+  k_scal<<<vec_ctas(n), VBS, 0, s>>>(a, f, n);
   LAUNCH_TAIL();
 }
 

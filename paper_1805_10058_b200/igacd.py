@@ -54,6 +54,7 @@ _aux_exact = _sig("igacd_aux_is_exact", [_vp, _P(_c_int)])
 _apply_aux = _sig("igacd_apply_aux", [_vp, _c_int, _vp, _vp, _vp])
 _aux_omega = _sig("igacd_aux_omega", [_vp, _c_int, _P(_c_double), _P(_c_double)])
 _solve = _sig("igacd_solve", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
+_gmres = _sig("igacd_gmres", [_vp, _vp, _vp, _c_double, _c_int, _c_int, _P(_c_int), _P(_c_double), _vp])
 _solve_host = _sig("igacd_solve_host", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
 _get_band = _sig("igacd_get_band", [_vp, _c_int, _c_int, _P(_c_double)])
 _get_prol = _sig("igacd_get_prolongation", [_vp, _c_int, _P(_c_double)])
@@ -64,6 +65,7 @@ _reset_prof = _sig("igacd_reset_profile", [_vp])
 IGACD_E_NOCONV = -4
 IGACD_PRECOND_VCYCLE = 0
 IGACD_PRECOND_AUX = 1
+IGACD_PRECOND_AUX_ADD = 2
 IGACD_SMOOTH_JACOBI = 0
 IGACD_SMOOTH_TOEPLITZ = 1
 
@@ -219,6 +221,14 @@ def igacd_aux_omega(h, level):
 def igacd_solve(h, b, x, tol, maxit, stream=None, raise_on_noconv=True):
     it, rel = _c_int(), _c_double()
     rc = _solve(h, _dptr(b), _dptr(x), tol, maxit, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
+    if rc != IGACD_E_NOCONV or raise_on_noconv:
+        _check(rc)
+    return it.value, rel.value
+
+
+def igacd_gmres(h, b, x, tol, maxit, restart=30, stream=None, raise_on_noconv=True):
+    it, rel = _c_int(), _c_double()
+    rc = _gmres(h, _dptr(b), _dptr(x), tol, maxit, restart, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
     if rc != IGACD_E_NOCONV or raise_on_noconv:
         _check(rc)
     return it.value, rel.value

@@ -370,3 +370,71 @@ def test_full_size_config_apply_sampled(ci):
         assert abs(lhs - rhs) <= 1e-11 * (abs(lhs) + abs(rhs))
     finally:
         ig.igacd_destroy(h)
+
+
+GMRES_CASES = [(Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels=2), 30),
+               (Case(3, 2, 8, nu=1.0, beta=0.1, levels=2), 30),
+               (Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)), 30),
+               (Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)), 7),
+               (Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0)), 5)]
+
+
+@pytest.mark.parametrize("case,restart", GMRES_CASES, ids=lambda v: repr(v))
+def test_gmres_matches_oracle(case, restart):
+    from oracle.krylov import fgmres
+    h = case.handle()
+    try:
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels)
+        b = np.random.default_rng(6).uniform(-1, 1, disc.ndof)
+        xo, ito, hist = fgmres(A, b, B, 1e-8, 3000, restart=restart)
+        x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        it, rel = ig.igacd_gmres(h, to_dev(b), x, 1e-8, 3000, restart=restart)
+        xg = to_host(x)
+        assert abs(it - ito) <= 1, (it, ito)
+        assert rel < 1e-8
+        assert np.linalg.norm(b - A @ xg) / np.linalg.norm(b) < 1e-8 * 1.5
+        assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-8
+    finally:
+        ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("case", [Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)),
+                                  Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0))], ids=repr)
+def test_additive_aux_preconditioner_and_solve(case):
+    h = case.handle()
+    try:
+        ig.igacd_set_preconditioner(h, ig.IGACD_PRECOND_AUX_ADD)
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels, mode="add")
+        b = np.random.default_rng(14).uniform(-1, 1, disc.ndof)
+        x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        ig.igacd_precond(h, to_dev(b), x)
+        # V r is applied to r itself (no damping by a following multiplicative step): its
+        # rounding error carries the coarsest level's conditioning (reading R9),
+        # tol = max(1e-12, 10 u kappa(A coarsest)); d2p3n64 (nu=1e-2, beta=1e-3): kappa = 1.4e5
+        tol = max(1e-12, 10 * np.finfo(float).eps * np.linalg.cond(B.V.A[-1].toarray()))
+        assert_close(to_host(x), B(b), tol, "additive aux precond")
+        xo, ito, _ = pcg(A, b, B, 1e-8, 3000)
+        x.zero_()
+        it, rel = ig.igacd_solve(h, to_dev(b), x, 1e-8, 3000)
+        assert abs(it - ito) <= 1 and rel < 1e-8
+        assert np.linalg.norm(to_host(x) - xo) / np.linalg.norm(xo) <= 1e-8
+    finally:
+        ig.igacd_destroy(h)
+
+
+def test_gmres_zero_rhs_and_arguments():
+    c = Case(2, 2, 8, levels=2)
+    h = c.handle()
+    try:
+        N = ig.igacd_ndof(h)
+        x = torch.ones(N, dtype=torch.float64, device="cuda")
+        it, rel = ig.igacd_gmres(h, torch.zeros(N, dtype=torch.float64, device="cuda"), x, 1e-8, 10)
+        assert it == 0 and float(x.abs().max()) == 0.0
+        with pytest.raises(ig.IgacdError):
+            ig.igacd_gmres(h, x, torch.zeros_like(x), 1e-8, 10, restart=0)
+    finally:
+        ig.igacd_destroy(h)

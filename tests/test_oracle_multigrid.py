@@ -150,3 +150,21 @@ def test_toeplitz_smoother_rho_and_fixed_point():
     assert 0.85 * lam <= H.rho_t[0] <= lam * (1 + 1e-10)
     x = np.random.default_rng(2).standard_normal(A.shape[0])
     assert np.max(np.abs(H.toeplitz(0, A @ x, x, 3) - x)) < 1e-12 * np.max(np.abs(x))
+
+
+def test_additive_aux_preconditioner_pins():
+    # R8' additive mode: symmetric, positive definite, and with the exact auxiliary solve
+    # (b0 = e1) it reproduces span{b0 s} exactly: B(A Pi s) - V(A Pi s) = Pi s.
+    c = inputs.config(0)
+    A = Discretization(c.dim, c.p, c.n).assemble(form_alfven(c.nu, c.beta, c.lam, c.b0))
+    B = AuxPreconditioner(A, c.dim, c.p, c.n, c.b0, c.levels, mode="add")
+    assert B.exact
+    rng = np.random.default_rng(8)
+    u, v = rng.standard_normal(A.shape[0]), rng.standard_normal(A.shape[0])
+    assert abs(u @ B(v) - v @ B(u)) <= 1e-10 * abs(u @ B(u))
+    assert u @ B(u) > 0 and v @ B(v) > 0
+    s = rng.standard_normal(A.shape[0] // c.dim)
+    r = A @ (B.Pi @ s)
+    assert np.max(np.abs(B(r) - B.V.vcycle(r) - B.Pi @ s)) <= 1e-10 * np.max(np.abs(s))
+    x, it, _ = pcg(A, inputs.rhs(c), B, c.tol, 500)
+    assert it < 60
