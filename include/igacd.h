@@ -91,10 +91,12 @@ int igacd_prolong(igacd_handle h, int level, const double* x_coarse, double* x_f
 int igacd_vcycle(igacd_handle h, const double* b, double* x, void* stream);
 
 /* The PCG preconditioner action x = B b (reading R8).  Mode IGACD_PRECOND_VCYCLE: B = V.
- * Mode IGACD_PRECOND_AUX (default when b0 != 0 and lambda > 0): symmetric multiplicative
+ * Mode IGACD_PRECOND_AUX (default in 2D when b0 != 0 and lambda > 0): symmetric multiplicative
  * combination of the auxiliary-space correction on span{b0 s} -- the kernel of the lambda
  * term -- with the V-cycle:  x = Pi Vs Pi^T b;  x += V(b - A x);  x += Pi Vs Pi^T (b - A x),
- * Pi s = b0 s, Vs = V-cycle of the scalar operator A_s = Pi^T A Pi on the same levels. */
+ * Pi s = b0 s, Vs = V-cycle of the scalar operator A_s = Pi^T A Pi on the same levels.
+ * Mode IGACD_PRECOND_AUX_ADD (default in 3D, reading R8'): x = V b + Pi Vs Pi^T b, the two
+ * terms computed concurrently on two streams. */
 #define IGACD_PRECOND_VCYCLE 0
 #define IGACD_PRECOND_AUX 1
 #define IGACD_PRECOND_AUX_ADD 2
@@ -138,6 +140,15 @@ int igacd_solve(igacd_handle h, const double* b, double* x, double tol, int maxi
  * Returns IGACD_E_NOCONV (x still written) when maxit is reached. */
 int igacd_gmres(igacd_handle h, const double* b, double* x, double tol, int maxit, int restart, int* iters,
                 double* relres, void* stream);
+
+/* igacd_solve replays each PCG iteration as two CUDA graphs (captured on first use, recaptured
+ * when x, the preconditioner or the smoother changes): A = operator + x/r update + ||r||^2,
+ * B = preconditioner + p update.  enable = 0 launches the same kernels one by one (results
+ * are bit-identical).  The environment variable IGACD_GRAPH=0 disables graphs globally. */
+/* Smoothing sweeps of the auxiliary scalar V-cycle (default: the handle's nu_pre / nu_post).
+ * IGACD_E_ARG when the handle has no auxiliary space. */
+int igacd_set_aux_sweeps(igacd_handle h, int nu_pre, int nu_post);
+int igacd_set_graphs(igacd_handle h, int enable);
 
 /* As igacd_solve with HOST b and x (pinned or pageable); the host<->device copies are
  * part of the call. */

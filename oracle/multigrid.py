@@ -154,8 +154,11 @@ class AuxPreconditioner:
     Bs = exact A_s^{-1} (sparse LU, library primitive) when b0 has exactly one nonzero
     component (A_s is then one Kronecker product), else the V-cycle of A_s."""
 
-    def __init__(self, A0, d, p, n, b0, levels=0, nu_pre=1, nu_post=1, smoother="toeplitz", mode="mult"):
+    def __init__(self, A0, d, p, n, b0, levels=0, nu_pre=1, nu_post=1, smoother="toeplitz", mode="mult",
+                 aux_nu_pre=None, aux_nu_post=None):
         assert mode in ("mult", "add")
+        aux_nu_pre = nu_pre if aux_nu_pre is None else aux_nu_pre
+        aux_nu_post = nu_post if aux_nu_post is None else aux_nu_post
         self.mode = mode
         self.A = sp.csr_matrix(A0)
         self.V = Hierarchy(A0, d, p, n, levels, nu_pre, nu_post, smoother=smoother)
@@ -166,7 +169,8 @@ class AuxPreconditioner:
             self.lu = spl.splu(As.tocsc())
             self.Bs = self.lu.solve
         else:
-            self.Vs = Hierarchy(As, d, p, n, levels, nu_pre, nu_post, ncomp=1, ns=self.V.ns, smoother=smoother)
+            self.Vs = Hierarchy(As, d, p, n, levels, aux_nu_pre, aux_nu_post, ncomp=1, ns=self.V.ns,
+                                smoother=smoother)
             self.Bs = self.Vs.vcycle
 
     def __call__(self, r):

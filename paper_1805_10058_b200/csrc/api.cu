@@ -124,6 +124,14 @@ static void destroy_handle(Handle* h) {
   for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar, h->zbuf}) cudaFree(v);
   for (double* v : {h->gm_v, h->gm_z, h->gm_partial, h->gm_dev}) cudaFree(v);
   if (h->gm_host) cudaFreeHost(h->gm_host);
+  if (h->gA) cudaGraphExecDestroy(h->gA);
+  if (h->gB) cudaGraphExecDestroy(h->gB);
+  if (h->ga0) cudaEventDestroy(h->ga0);
+  if (h->ga1) cudaEventDestroy(h->ga1);
+  if (h->cap) cudaStreamDestroy(h->cap);
+  if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (auto& pr : h->ev_pending) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
@@ -198,6 +206,8 @@ static void setup_system(Handle& h, int sy, int nc, const Coef& coef, cudaStream
   System& S = h.sys[sy];
   S.nc = nc;
   S.coef = coef;
+  S.nu_pre = h.nu_pre;
+  S.nu_post = h.nu_post;
   S.lv.resize(h.lv.size());
   for (size_t l = 0; l < h.lv.size(); ++l) {
     SysLevel& L = S.lv[l];
@@ -321,7 +331,8 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
       setup_system(*h, 1, 1, ac, s);
       setup_aux_tensor(*h, s);
     }
-    h->precond = h->has_aux ? PRECOND_AUX : PRECOND_VCYCLE;
+    // reading R8': additive in 3D, multiplicative in 2D (measured time-to-solution)
+    h->precond = h->has_aux ? (dim == 3 ? PRECOND_AUX_ADD : PRECOND_AUX) : PRECOND_VCYCLE;
     IGACD_CUDA(cudaStreamSynchronize(s));
   } catch (...) {
     destroy_handle(h);
@@ -388,10 +399,10 @@ static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, c
     return;
   }
   SysLevel& L = S.lv[l];
-  const int swaps = h.smoother == SMOOTH_JACOBI ? std::max(0, h.nu_pre - 1) + h.nu_post : 0;
+  const int swaps = h.smoother == SMOOTH_JACOBI ? std::max(0, S.nu_pre - 1) + S.nu_post : 0;
   double* cur = (swaps % 2 == 0) ? x : L.t;
   double* oth = (cur == x) ? L.t : x;
-  smooth(h, sy, l, b, cur, oth, h.nu_pre, true, s);
+  smooth(h, sy, l, b, cur, oth, S.nu_pre, true, s);
   Epi ep{};
   ep.b = b;
   launch_operator(h, sy, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
@@ -399,7 +410,7 @@ static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, c
   launch_restrict(h, S.nc, l, L.r, C.b, s);
   vcycle_level(h, sy, l + 1, C.b, C.x, s);
   launch_prolong(h, S.nc, l, C.x, cur, true, s);
-  smooth(h, sy, l, b, cur, oth, h.nu_post, false, s);
+  smooth(h, sy, l, b, cur, oth, S.nu_post, false, s);
   if (cur != x) launch_copy(h, cur, x, L.ndof, s);
 }
 
@@ -427,10 +438,21 @@ static void precond_apply(Handle& h, const double* r, double* z, cudaStream_t s)
   SysLevel& a0 = A.lv[0];
   Epi ep{};
   ep.b = r;
-  if (h.precond == PRECOND_AUX_ADD) {   // additive: z = V r + Pi B_s Pi^T r
+  if (h.precond == PRECOND_AUX_ADD) {   // additive (R8'): z = V r + Pi B_s Pi^T r
+    // the two corrections are independent: the scalar branch runs on a second stream
+    // (fork/join events; captured as parallel graph branches)
+    if (!h.aux_stream) {
+      IGACD_CUDA(cudaStreamCreateWithFlags(&h.aux_stream, cudaStreamNonBlocking));
+      IGACD_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
+      IGACD_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
+    }
+    IGACD_CUDA(cudaEventRecord(h.ev_fork, s));
+    IGACD_CUDA(cudaStreamWaitEvent(h.aux_stream, h.ev_fork, 0));
+    launch_pi_t(h, r, a0.b, h.aux_stream);
+    aux_solve(h, a0.b, a0.x, h.aux_stream);
+    IGACD_CUDA(cudaEventRecord(h.ev_join, h.aux_stream));
     vcycle_level(h, 0, 0, r, z, s);
-    launch_pi_t(h, r, a0.b, s);
-    aux_solve(h, a0.b, a0.x, s);
+    IGACD_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
     launch_pi(h, a0.x, z, true, s);
     return;
   }
@@ -447,10 +469,90 @@ static void precond_apply(Handle& h, const double* r, double* z, cudaStream_t s)
 }
 
 // ---- PCG ---------------------------------------------------------------------------------
+// Textbook PCG (R7; oracle krylov.pcg) with device-side scalars in fixed slots:
+//   A:  q = A p, (p, q) -> pq;  x += alpha p, r -= alpha q (alpha = rz/pq), ||r||^2 -> host
+//   B:  z = B r, (r, z) -> rz';  p = z + (rz'/rz) p;  rz <- rz'
+// The host reads ||r||^2 after A (the stopping test) and launches B only when
+// the iteration continues.  A and B are captured once as CUDA graphs (IGACD_GRAPH=0 runs the
+// same kernels eagerly), so an iteration costs two graph launches and one host sync.
+static bool graphs_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IGACD_GRAPH");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static void graphs_reset(Handle& h) {
+  if (h.gA) cudaGraphExecDestroy(h.gA);
+  if (h.gB) cudaGraphExecDestroy(h.gB);
+  h.gA = h.gB = nullptr;
+  h.g_x = nullptr;
+}
+
+template <class F>
+static cudaGraphExec_t capture(Handle& h, F&& body, long long* nk) {
+  if (!h.cap) IGACD_CUDA(cudaStreamCreateWithFlags(&h.cap, cudaStreamNonBlocking));
+  const long long before = h.launches;
+  IGACD_CUDA(cudaStreamBeginCapture(h.cap, cudaStreamCaptureModeThreadLocal));
+  cudaGraph_t g = nullptr;
+  try {
+    body(h.cap);
+  } catch (...) {
+    cudaStreamEndCapture(h.cap, &g);
+    if (g) cudaGraphDestroy(g);
+    h.launches = before;
+    throw;
+  }
+  IGACD_CUDA(cudaStreamEndCapture(h.cap, &g));
+  cudaGraphExec_t ex = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  IGACD_CUDA(e);
+  *nk = h.launches - before;
+  h.launches = before;
+  return ex;
+}
+
+// an event record that becomes an event node when `s` is being captured
+static void record_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  IGACD_CUDA(cudaStreamIsCapturing(s, &st));
+  if (st == cudaStreamCaptureStatusActive) IGACD_CUDA(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal));
+  else IGACD_CUDA(cudaEventRecord(ev, s));
+}
+
+static void pcg_part_a(Handle& h, double* x, cudaStream_t s) {
+  const size_t N = h.sys[0].lv[0].ndof;
+  Epi ep{};
+  ep.partial = h.partial;
+  record_event(h.ga0, s);
+  const int np = launch_operator(h, 0, 0, h.pp, h.pq, EPI_APPLY, DOT_X_OUT, ep, s);
+  record_event(h.ga1, s);
+  launch_finalize(h, h.partial, np, h.scal + S_PQ, s);
+  launch_pcg_update_xr(h, x, h.pr, h.pp, h.pq, N, h.scal + S_RZ0, h.scal + S_PQ, h.partial, s);
+  launch_finalize(h, h.partial, vec_ctas(N), h.scal + S_RR, s);
+  IGACD_CUDA(cudaMemcpyAsync(h.hscal + S_RR, h.scal + S_RR, sizeof(double), cudaMemcpyDeviceToHost, s));
+}
+
+static void pcg_part_b(Handle& h, cudaStream_t s) {
+  const size_t N = h.sys[0].lv[0].ndof;
+  precond_apply(h, h.pr, h.pz, s);
+  launch_dot(h, h.pr, h.pz, N, h.partial, s);
+  launch_finalize(h, h.partial, vec_ctas(N), h.scal + S_RZ1, s);
+  launch_pcg_update_p(h, h.pp, h.pz, N, h.scal + S_RZ1, h.scal + S_RZ0, s);
+  IGACD_CUDA(cudaMemcpyAsync(h.scal + S_RZ0, h.scal + S_RZ1, sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
 static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
                cudaStream_t s) {
   const size_t N = h.sys[0].lv[0].ndof;
   const int nv = vec_ctas(N);
+  if (!h.ga0) {
+    IGACD_CUDA(cudaEventCreate(&h.ga0));
+    IGACD_CUDA(cudaEventCreate(&h.ga1));
+  }
   launch_copy(h, b, h.pr, N, s);
   launch_dot(h, h.pr, h.pr, N, h.partial, s);
   const double rr0 = reduce_to_host(h, nv, S_RR, s);
@@ -459,57 +561,47 @@ static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int
   if (iters) *iters = 0;
   if (relres) *relres = 0.0;
   if (r0 == 0.0) return IGACD_OK;
+  // first preconditioner application eagerly (also initialises every kernel's attributes)
   precond_apply(h, h.pr, h.pz, s);
   launch_dot(h, h.pr, h.pz, N, h.partial, s);
-  int rz = S_RZ0;
-  launch_finalize(h, h.partial, nv, h.scal + rz, s);
+  launch_finalize(h, h.partial, nv, h.scal + S_RZ0, s);
   launch_copy(h, h.pz, h.pp, N, s);
-  Epi ep{};
-  ep.partial = h.partial;
+  const bool use_graph = h.graphs && graphs_enabled();
+  if (use_graph && h.g_x != x) {
+    graphs_reset(h);
+    h.gA = capture(h, [&](cudaStream_t cs) { pcg_part_a(h, x, cs); }, &h.nA);
+    h.gB = capture(h, [&](cudaStream_t cs) { pcg_part_b(h, cs); }, &h.nB);
+    h.g_x = x;
+  }
   double rel = 1.0;
   int it = 0;
   for (it = 1; it <= maxit; ++it) {
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h.profiling) {
-      IGACD_CUDA(cudaEventCreate(&e0));
-      IGACD_CUDA(cudaEventCreate(&e1));
-      IGACD_CUDA(cudaEventRecord(e0, s));
+    if (use_graph) {
+      IGACD_CUDA(cudaGraphLaunch(h.gA, s));
+      h.launches += h.nA;
+    } else {
+      pcg_part_a(h, x, s);
     }
-    const int np = launch_operator(h, 0, 0, h.pp, h.pq, EPI_APPLY, DOT_X_OUT, ep, s);
+    IGACD_CUDA(cudaStreamSynchronize(s));
     h.apply_launches++;
     if (h.profiling) {
-      IGACD_CUDA(cudaEventRecord(e1, s));
-      h.ev_pending.push_back({e0, e1});
-    }
-    launch_finalize(h, h.partial, np, h.scal + S_PQ, s);
-    launch_pcg_update_xr(h, x, h.pr, h.pp, h.pq, N, h.scal + rz, h.scal + S_PQ, h.partial, s);
-    const double rr = reduce_to_host(h, nv, S_RR, s);
-    rel = std::sqrt(rr) / r0;
-    if (rel < tol) break;
-    if (it == maxit) break;
-    precond_apply(h, h.pr, h.pz, s);
-    launch_dot(h, h.pr, h.pz, N, h.partial, s);
-    const int rzn = rz == S_RZ0 ? S_RZ1 : S_RZ0;
-    launch_finalize(h, h.partial, nv, h.scal + rzn, s);
-    launch_pcg_update_p(h, h.pp, h.pz, N, h.scal + rzn, h.scal + rz, s);
-    rz = rzn;
-  }
-  if (h.profiling) {
-    IGACD_CUDA(cudaStreamSynchronize(s));
-    for (auto& pr : h.ev_pending) {
       float ms = 0.f;
-      IGACD_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      IGACD_CUDA(cudaEventElapsedTime(&ms, h.ga0, h.ga1));
       h.apply_ms += ms;
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
     }
-    h.ev_pending.clear();
+    rel = std::sqrt(h.hscal[S_RR]) / r0;
+    if (rel < tol || it == maxit) break;
+    if (use_graph) {
+      IGACD_CUDA(cudaGraphLaunch(h.gB, s));
+      h.launches += h.nB;
+    } else {
+      pcg_part_b(h, s);
+    }
   }
   if (iters) *iters = std::min(it, maxit);
   if (relres) *relres = rel;
   return rel < tol ? IGACD_OK : IGACD_E_NOCONV;
 }
-
 
 // ---- FGMRES ------------------------------------------------------------------------------
 // Flexible right-preconditioned GMRES(restart) (the paper's PGMRES; oracle
@@ -825,6 +917,7 @@ int igacd_set_preconditioner(igacd_handle h, int mode) {
   if (mode != PRECOND_VCYCLE && mode != PRECOND_AUX && mode != PRECOND_AUX_ADD)
     throw Error{IGACD_E_ARG, "unknown preconditioner"};
   if (mode != PRECOND_VCYCLE && !hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space (b0 = 0 or lambda = 0)"};
+  if (hh->precond != mode) graphs_reset(*hh);
   hh->precond = mode;
   API_END
 }
@@ -832,7 +925,27 @@ int igacd_set_preconditioner(igacd_handle h, int mode) {
 int igacd_set_smoother(igacd_handle h, int kind) {
   API_BEGIN
   if (kind != SMOOTH_JACOBI && kind != SMOOTH_TOEPLITZ) throw Error{IGACD_E_ARG, "unknown smoother"};
+  if (H(h)->smoother != kind) graphs_reset(*H(h));
   H(h)->smoother = kind;
+  API_END
+}
+
+int igacd_set_aux_sweeps(igacd_handle h, int nu_pre, int nu_post) {
+  API_BEGIN
+  Handle* hh = H(h);
+  if (!hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space on this handle"};
+  if (nu_pre < 0 || nu_post < 0) throw Error{IGACD_E_ARG, "negative sweep count"};
+  graphs_reset(*hh);
+  hh->sys[1].nu_pre = nu_pre;
+  hh->sys[1].nu_post = nu_post;
+  API_END
+}
+
+int igacd_set_graphs(igacd_handle h, int enable) {
+  API_BEGIN
+  Handle* hh = H(h);
+  if ((enable != 0) != hh->graphs) graphs_reset(*hh);
+  hh->graphs = enable != 0;
   API_END
 }
 

@@ -99,6 +99,7 @@ struct SysLevel {
 // auxiliary scalar operator A_s = Pi^T A Pi on span{b0 s} (nc = 1), reading R8.
 struct System {
   int nc = 0;
+  int nu_pre = 1, nu_post = 1;   // smoothing sweeps of this system's V-cycle
   Coef coef;
   std::vector<SysLevel> lv;
   double* cinv = nullptr;   // dense inverse of the coarsest level
@@ -121,8 +122,8 @@ struct Handle {
   int precond = PRECOND_VCYCLE;
   int smoother = SMOOTH_TOEPLITZ;
   // transfer scratch (max size), reductions
-  double* scratch0 = nullptr;
-  double* scratch1 = nullptr;
+  double* scratch0 = nullptr;   // vector-system transfers
+  double* scratch1 = nullptr;   // scalar-system transfers (the additive branch runs concurrently)
   size_t scratch_len = 0;
   double* partial = nullptr;    // per-CTA partial sums
   size_t partial_len = 0;
@@ -140,6 +141,16 @@ struct Handle {
   double* gm_dev = nullptr;       // [h1 (r+1) | h2 (r+1) | ||w||^2 | y (r)]
   double* gm_host = nullptr;      // pinned mirror
   cudaStream_t stream = nullptr;
+  // CUDA graphs of the PCG iteration (api.cu): A = apply + x/r update + ||r||^2 -> host,
+  // B = preconditioner + (r, z) + p update; captured on `cap`, replayed on the caller's stream
+  cudaStream_t aux_stream = nullptr;          // concurrent branch of the additive preconditioner
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool graphs = true;               // igacd_set_graphs (and IGACD_GRAPH=0 in the environment)
+  cudaStream_t cap = nullptr;
+  cudaGraphExec_t gA = nullptr, gB = nullptr;
+  long long nA = 0, nB = 0;         // kernels per replay
+  const double* g_x = nullptr;      // solution pointer baked into gA
+  cudaEvent_t ga0 = nullptr, ga1 = nullptr;   // apply timing inside gA
   // instrumentation
   long long launches = 0, apply_launches = 0;
   double apply_ms = 0.0;

@@ -159,8 +159,9 @@ void launch_prolong(Handle& h, int nc, int level, const double* xc, double* xf, 
     transfer2d(h, xc, xf, d, (int)mc, (int)mf, T.p_start, T.p_w, T.wp, T.pwin1, T.pwin2, accumulate, s);
   } else {
     // axis 0: [d][mc][mc][mc] -> [d][mf][mc][mc]; axes 1, 2 per slab: -> [d][mf][mf][mf]
-    axis_pass(h, xc, h.scratch0, d, (int)mc, (int)mf, mc * mc, T.p_start, T.p_w, T.wp, false, s);
-    transfer2d(h, h.scratch0, xf, d * mf, (int)mc, (int)mf, T.p_start, T.p_w, T.wp, T.pwin1, T.pwin2, accumulate, s);
+    double* scr = nc == 1 ? h.scratch1 : h.scratch0;   // the scalar system may run concurrently
+    axis_pass(h, xc, scr, d, (int)mc, (int)mf, mc * mc, T.p_start, T.p_w, T.wp, false, s);
+    transfer2d(h, scr, xf, d * mf, (int)mc, (int)mf, T.p_start, T.p_w, T.wp, T.pwin1, T.pwin2, accumulate, s);
   }
 }
 
@@ -171,8 +172,9 @@ void launch_restrict(Handle& h, int nc, int level, const double* xf, double* xc,
     transfer2d(h, xf, xc, d, (int)mf, (int)mc, T.r_start, T.r_w, T.wr, T.rwin1, T.rwin2, false, s);
   } else {
     // axes 1, 2 per fine slab: [d][mf][mf][mf] -> [d][mf][mc][mc]; axis 0: -> [d][mc][mc][mc]
-    transfer2d(h, xf, h.scratch0, d * mf, (int)mf, (int)mc, T.r_start, T.r_w, T.wr, T.rwin1, T.rwin2, false, s);
-    axis_pass(h, h.scratch0, xc, d, (int)mf, (int)mc, mc * mc, T.r_start, T.r_w, T.wr, false, s);
+    double* scr = nc == 1 ? h.scratch1 : h.scratch0;
+    transfer2d(h, xf, scr, d * mf, (int)mf, (int)mc, T.r_start, T.r_w, T.wr, T.rwin1, T.rwin2, false, s);
+    axis_pass(h, scr, xc, d, (int)mf, (int)mc, mc * mc, T.r_start, T.r_w, T.wr, false, s);
   }
 }
 

@@ -29,6 +29,11 @@ S2, S3 = 2 ** -0.5, 3 ** -0.5
 PARAMS = dict(nu=0.3, beta=0.05, lam=1.0)
 
 
+def default_mode(d):
+    """The library's default auxiliary combination (reading R8'): additive in 3D."""
+    return "add" if d == 3 else "mult"
+
+
 def b0_for(d):
     return (0.6, 0.8) if d == 2 else (0.48, 0.6, 0.64)
 
@@ -251,7 +256,9 @@ def test_aux_preconditioner_matches_oracle(case):
         disc = Discretization(case.d, case.p, case.n)
         A = disc.assemble(case.form)
         B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels)
-        assert ig.igacd_get_preconditioner(h) == ig.IGACD_PRECOND_AUX
+        # default: multiplicative in 2D, additive in 3D (reading R8'); test the multiplicative here
+        assert ig.igacd_get_preconditioner(h) == (ig.IGACD_PRECOND_AUX if case.d == 2 else ig.IGACD_PRECOND_AUX_ADD)
+        ig.igacd_set_preconditioner(h, ig.IGACD_PRECOND_AUX)
         assert ig.igacd_aux_is_exact(h) == int(B.exact)
         if not B.exact:
             for l in range(len(B.Vs.ns) - 1):
@@ -277,7 +284,7 @@ def test_solve_matches_oracle(case):
     try:
         disc = Discretization(case.d, case.p, case.n)
         A = disc.assemble(case.form)
-        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels)
+        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels, mode=default_mode(case.d))
         b = np.random.default_rng(5).uniform(-1, 1, disc.ndof)
         xo, ito, hist = pcg(A, b, B, 1e-8, 2000)
         x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
@@ -386,7 +393,7 @@ def test_gmres_matches_oracle(case, restart):
     try:
         disc = Discretization(case.d, case.p, case.n)
         A = disc.assemble(case.form)
-        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels)
+        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels, mode=default_mode(case.d))
         b = np.random.default_rng(6).uniform(-1, 1, disc.ndof)
         xo, ito, hist = fgmres(A, b, B, 1e-8, 3000, restart=restart)
         x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
@@ -436,5 +443,23 @@ def test_gmres_zero_rhs_and_arguments():
         assert it == 0 and float(x.abs().max()) == 0.0
         with pytest.raises(ig.IgacdError):
             ig.igacd_gmres(h, x, torch.zeros_like(x), 1e-8, 10, restart=0)
+    finally:
+        ig.igacd_destroy(h)
+
+
+def test_graph_replay_is_bit_identical_to_eager_launches():
+    case = Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0))
+    h = case.handle()
+    try:
+        N = ig.igacd_ndof(h)
+        b = to_dev(np.random.default_rng(21).uniform(-1, 1, N))
+        xg = torch.zeros(N, dtype=torch.float64, device="cuda")
+        xe = torch.zeros_like(xg)
+        itg, relg = ig.igacd_solve(h, b, xg, 1e-8, 2000)
+        itg2, _ = ig.igacd_solve(h, b, xg, 1e-8, 2000)      # replay of the cached graphs
+        ig.igacd_set_graphs(h, False)
+        ite, rele = ig.igacd_solve(h, b, xe, 1e-8, 2000)
+        assert itg == itg2 == ite and relg == rele
+        assert torch.equal(xg, xe)
     finally:
         ig.igacd_destroy(h)
