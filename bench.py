@@ -113,7 +113,7 @@ def cpu_sample(cfg):
     small = cfg.with_(n=n, levels=0)
     if small not in _CPU_CACHE:
         A = Discretization(small.dim, small.p, small.n).assemble(form_alfven(small.nu, small.beta, small.lam, small.b0))
-        mode = "add" if small.dim == 3 else "mult"   # the library default (reading R8')
+        mode = "add"   # the library default (reading R8')
         _CPU_CACHE[small] = (A, AuxPreconditioner(A, small.dim, small.p, small.n, small.b0, small.levels, mode=mode))
     A, B = _CPU_CACHE[small]
     b = inputs.rhs(small)

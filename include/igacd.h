@@ -91,12 +91,12 @@ int igacd_prolong(igacd_handle h, int level, const double* x_coarse, double* x_f
 int igacd_vcycle(igacd_handle h, const double* b, double* x, void* stream);
 
 /* The PCG preconditioner action x = B b (reading R8).  Mode IGACD_PRECOND_VCYCLE: B = V.
- * Mode IGACD_PRECOND_AUX (default in 2D when b0 != 0 and lambda > 0): symmetric multiplicative
+ * Mode IGACD_PRECOND_AUX: symmetric multiplicative
  * combination of the auxiliary-space correction on span{b0 s} -- the kernel of the lambda
  * term -- with the V-cycle:  x = Pi Vs Pi^T b;  x += V(b - A x);  x += Pi Vs Pi^T (b - A x),
  * Pi s = b0 s, Vs = V-cycle of the scalar operator A_s = Pi^T A Pi on the same levels.
- * Mode IGACD_PRECOND_AUX_ADD (default in 3D, reading R8'): x = V b + Pi Vs Pi^T b, the two
- * terms computed concurrently on two streams. */
+ * Mode IGACD_PRECOND_AUX_ADD (the default when b0 != 0 and lambda > 0, reading R8'):
+ * x = V b + Pi Vs Pi^T b, the two terms computed concurrently on two streams. */
 #define IGACD_PRECOND_VCYCLE 0
 #define IGACD_PRECOND_AUX 1
 #define IGACD_PRECOND_AUX_ADD 2

@@ -331,8 +331,8 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
       setup_system(*h, 1, 1, ac, s);
       setup_aux_tensor(*h, s);
     }
-    // reading R8': additive in 3D, multiplicative in 2D (measured time-to-solution)
-    h->precond = h->has_aux ? (dim == 3 ? PRECOND_AUX_ADD : PRECOND_AUX) : PRECOND_VCYCLE;
+    // reading R8': the concurrent additive combination (measured time-to-solution)
+    h->precond = h->has_aux ? PRECOND_AUX_ADD : PRECOND_VCYCLE;
     IGACD_CUDA(cudaStreamSynchronize(s));
   } catch (...) {
     destroy_handle(h);

@@ -67,6 +67,7 @@ struct BandFactor {
   double* Lb = nullptr;    // [m][w+1]: L[k][k-j] at k*(w+1) + (w-j)
   double* inv = nullptr;   // [m]: 1/L[k][k]
   double* fac = nullptr;   // [(2(w+1)+1) m]: scaled forward/backward coefficients and 1/L[k][k] (tiled kernel)
+  int kc = 0;              // rows k >= kc of L (and 1/L[k][k]) are bitwise equal to the last row
   void upload(const std::vector<double>& Lb_h, const std::vector<double>& inv_h, int m_, int w_);
   void release();
 };

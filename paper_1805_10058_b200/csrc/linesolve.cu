@@ -77,77 +77,66 @@ __device__ __forceinline__ void ls_cp_async8(double* smem_dst, const double* gsr
 //   acc[q] (row t+1+q) -= G[t][q] v_t,  q = 0..W-1,
 // where forward G[t][q] = i_r L[r][t] (r = t+1+q) and backward G[t][q] = i_r L[k][r]
 // (k = m-1-t, r = k-1-q), and row t+W enters the ring as i_r * tile[r].  The loop-carried
-// dependency is one DFMA per step (acc[1] - G v_t -> next v).  Steps run in blocks of D (a
-// multiple of W, so the ring maps back onto itself); the shared-memory operands of block b+1
-// are loaded into the other of two register sets while block b is processed.
-template <int W>
-struct SweepSet {
-  static constexpr int D = W >= 3 ? W : W * ((4 + W - 1) / W);
-  double g[D][W], tv[D], iv[D];
-};
-
-// tile and sI carry W zero rows below 0 and above m-1, so the entering row t+W needs no guard
+// dependency is one DFMA per step (acc[1] - G v_t -> next v).
+// The rows of the Cholesky factor of T(m_{p-1}) become bitwise constant from row Kc on
+// (BandFactor::kc): on the steps whose operands all come from those rows, G[t][q] and i_r are
+// the same numbers for every t, so they are held in registers (no shared-memory operand
+// loads) and the entering rows are read 8 steps ahead; the first / last rows use the tables.
 template <int W, int TP, bool FWD>
-__device__ __forceinline__ void sweep_load(SweepSet<W>& S, const double* tile, const double* __restrict__ G,
-                                           const double* sI, int m, int t0) {
-  constexpr int D = SweepSet<W>::D;
-  const int r0 = FWD ? t0 + W : m - 1 - t0 - W;
-  const double* tb = tile + r0 * TP;
-  const double* ib = sI + r0;
-  const double* gb = G + t0 * (W + 1);
-#pragma unroll
-  for (int u = 0; u < D; ++u) {
-#pragma unroll
-    for (int q = 0; q < W; ++q) S.g[u][q] = gb[u * (W + 1) + q];
-    S.tv[u] = tb[FWD ? u * TP : -u * TP];
-    S.iv[u] = ib[FWD ? u : -u];
-  }
-}
-
-template <int W, int TP, bool FWD>
-__device__ __forceinline__ void sweep_block(const SweepSet<W>& S, double (&acc)[W], double* tile, int m, int t0) {
-  constexpr int D = SweepSet<W>::D;
-  double* tb = tile + (FWD ? t0 : m - 1 - t0) * TP;
-#pragma unroll
-  for (int u = 0; u < D; ++u) {
-    const double v = acc[0];
-    const double enter = S.tv[u] * S.iv[u];
-#pragma unroll
-    for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-S.g[u][q], v, acc[q + 1]);
-    acc[W - 1] = fma(-S.g[u][W - 1], v, enter);
-    tb[FWD ? u * TP : -u * TP] = v;
-  }
-}
-
-// `tile` points at this lane's element 0 (stride TP); `sI` at 1/L[0][0]; both padded by W zero rows
-template <int W, int TP, bool FWD>
-__device__ __forceinline__ void band_sweep(double* tile, const double* __restrict__ G, const double* sI, int m) {
+__device__ __forceinline__ void band_sweep(double* tile, const double* __restrict__ G, const double* sI, int m,
+                                           int kc) {
   auto row = [&](int t) { return FWD ? t : m - 1 - t; };
   if constexpr (W == 0) {
     for (int t = 0; t < m; ++t) tile[t * TP] *= sI[t];
   } else {
-    constexpr int D = SweepSet<W>::D;
     double acc[W];
 #pragma unroll
     for (int q = 0; q < W; ++q) acc[q] = tile[row(q) * TP] * sI[row(q)];
-    const int nb = m / D;
-    SweepSet<W> s0, s1;
-    if (nb > 0) sweep_load<W, TP, FWD>(s0, tile, G, sI, m, 0);
-    for (int b = 0; b < nb; b += 2) {
-      if (b + 1 < nb) sweep_load<W, TP, FWD>(s1, tile, G, sI, m, (b + 1) * D);
-      sweep_block<W, TP, FWD>(s0, acc, tile, m, b * D);
-      if (b + 1 >= nb) break;
-      if (b + 2 < nb) sweep_load<W, TP, FWD>(s0, tile, G, sI, m, (b + 2) * D);
-      sweep_block<W, TP, FWD>(s1, acc, tile, m, (b + 1) * D);
-    }
-    for (int t = nb * D; t < m; ++t) {   // tail: fewer than D steps
-      const double v = acc[0];
-      const double enter = tile[row(t + W) * TP] * sI[row(t + W)];
+    auto generic = [&](int t0, int t1) {
+      for (int t = t0; t < t1; ++t) {
+        const double v = acc[0];
+        const double enter = tile[row(t + W) * TP] * sI[row(t + W)];
 #pragma unroll
-      for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-G[t * (W + 1) + q], v, acc[q + 1]);
-      acc[W - 1] = fma(-G[t * (W + 1) + W - 1], v, enter);
+        for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-G[t * (W + 1) + q], v, acc[q + 1]);
+        acc[W - 1] = fma(-G[t * (W + 1) + W - 1], v, enter);
+        tile[row(t) * TP] = v;
+      }
+    };
+    int ta = FWD ? kc : 0;
+    int tb = FWD ? m - W : m - W - kc;
+    if (ta >= tb) {
+      generic(0, m);
+      return;
+    }
+    generic(0, ta);
+    double gc[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) gc[q] = G[ta * (W + 1) + q];
+    const double ic = sI[row(ta + W)];
+    constexpr int U = 8;
+    int t = ta;
+    for (; t + U <= tb; t += U) {
+      double e[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) e[u] = tile[row(t + W + u) * TP];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double v = acc[0];
+#pragma unroll
+        for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-gc[q], v, acc[q + 1]);
+        acc[W - 1] = fma(-gc[W - 1], v, e[u] * ic);
+        tile[row(t + u) * TP] = v;
+      }
+    }
+    for (; t < tb; ++t) {
+      const double v = acc[0];
+      const double enter = tile[row(t + W) * TP] * ic;
+#pragma unroll
+      for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-gc[q], v, acc[q + 1]);
+      acc[W - 1] = fma(-gc[W - 1], v, enter);
       tile[row(t) * TP] = v;
     }
+    generic(tb, m);
   }
 }
 
@@ -160,7 +149,8 @@ __device__ __forceinline__ void band_sweep(double* tile, const double* __restric
 template <int W, int WARPS, int TW, int NBUF>
 __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restrict__ data, long long outer, int m,
                                                                long long inner, const double* __restrict__ fac,
-                                                               int mode, double omega, double* __restrict__ xacc) {
+                                                               int kc, int mode, double omega,
+                                                               double* __restrict__ xacc) {
   extern __shared__ __align__(16) double sh[];
   double* sF = sh;                          // [m][W+1]: forward column table (BandFactor::fac)
   double* sB = sF + (size_t)m * (W + 1);    // [m][W+1]: backward column table
@@ -211,28 +201,52 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
-  // store (or accumulate omega * result into xacc, reading xacc U elements ahead so the
-  // read-modify-writes overlap instead of serialising on DRAM latency)
+  // store the solved tile (mode 0) or accumulate omega * result into xacc (mode 1).
+  // Mode 1 on contiguous lines (the last axis): x_acc += omega * result, with x_acc read in
+  // batches of UA per lane; batch 0 is requested before the sweeps (its latency hides behind
+  // them) and batch b+1 is in flight while batch b is stored.
+  constexpr int UA = 24;
+  double xa0[UA], xa1[UA];
+  auto acc_load = [&](const double* src, int e0, int tot, double (&xv)[UA]) {
+#pragma unroll
+    for (int u = 0; u < UA; ++u) xv[u] = (e0 + 32 * u < tot) ? src[e0 + 32 * u] : 0.0;
+  };
   auto store = [&](long long g, const double* tile) {
     const long long l0 = g * TW;
     const int nl = (int)min((long long)TW, lines - l0);
     constexpr int U = 16;
-    if (inner == 1) {
-      double* dst = (mode == 0 ? data : xacc) + l0 * m;
+    if (inner == 1 && mode != 0) {
+      double* dst = xacc + l0 * m;
+      const int tot = nl * m;
+      int k = lane % m, ln = lane / m;
+      auto put = [&](int e0, const double (&xv)[UA]) {
+#pragma unroll
+        for (int u = 0; u < UA; ++u) {
+          const int e = e0 + 32 * u;
+          if (e < tot) {
+            dst[e] = fma(omega, tile[k * TP + ln], xv[u]);
+            k += 32;
+            while (k >= m) { k -= m; ++ln; }
+          }
+        }
+      };
+      for (int e0 = lane; e0 < tot; e0 += 64 * UA) {   // xa0 holds batch e0 (loaded earlier)
+        if (e0 + 32 * UA < tot) acc_load(dst, e0 + 32 * UA, tot, xa1);
+        put(e0, xa0);
+        if (e0 + 32 * UA >= tot) break;
+        if (e0 + 64 * UA < tot) acc_load(dst, e0 + 64 * UA, tot, xa0);
+        put(e0 + 32 * UA, xa1);
+      }
+    } else if (inner == 1) {
+      double* dst = data + l0 * m;
       const int tot = nl * m;
       int k = lane % m, ln = lane / m;
       for (int e0 = lane; e0 < tot; e0 += 32 * U) {
-        double xv[U];
-        if (mode != 0) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) xv[u] = (e0 + 32 * u < tot) ? dst[e0 + 32 * u] : 0.0;
-        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int e = e0 + 32 * u;
           if (e < tot) {
-            const double v = tile[k * TP + ln];
-            dst[e] = mode == 0 ? v : fma(omega, v, xv[u]);
+            dst[e] = tile[k * TP + ln];
             k += 32;
             while (k >= m) { k -= m; ++ln; }
           }
@@ -286,11 +300,12 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
     }
     __syncwarp();
     const int nl = (int)min((long long)TW, lines - g * TW);
+    if (inner == 1 && mode != 0) acc_load(xacc + g * TW * m, lane, nl * m, xa0);   // batch 0, ahead
     if (lane < nl) {
       // forward  y_k = i_k b_k - sum_j (i_k L[k][k-j]) y_{k-j}
       // backward x_k = i_k y_k - sum_j (i_k L[k+j][k]) x_{k+j}
-      band_sweep<W, TP, true>(tile + lane, sF, sI, m);
-      band_sweep<W, TP, false>(tile + lane, sB, sI, m);
+      band_sweep<W, TP, true>(tile + lane, sF, sI, m, kc);
+      band_sweep<W, TP, false>(tile + lane, sB, sI, m, kc);
     }
     __syncwarp();
     store(g, tile);
@@ -343,6 +358,14 @@ void BandFactor::upload(const std::vector<double>& Lb_h, const std::vector<doubl
       if (rb >= 0) Gb[(size_t)t * (w + 1) + q] = inv_h[rb] * Lh(k, rb);
     }
   }
+  // first row from which every row of L (and 1/L[k][k]) equals the last row bit for bit
+  kc = m;
+  for (int k = m - 1; k >= 0; --k) {
+    bool same = inv_h[k] == inv_h[m - 1];
+    for (int j = 0; j <= w && same; ++j) same = Lb_h[(size_t)k * (w + 1) + j] == Lb_h[(size_t)(m - 1) * (w + 1) + j];
+    if (!same) break;
+    kc = k;
+  }
   IGACD_CUDA(cudaMalloc(&fac, sizeof(double) * f.size()));
   IGACD_CUDA(cudaMemcpy(fac, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice));
 }
@@ -390,7 +413,7 @@ static bool try_tiled(double* data, long long outer, int m, long long inner, con
   }
   blocks = std::min<long long>(blocks, (long long)occ * num_sms());
   k_band_solve_tiled<W, WARPS, TW, NBUF><<<(unsigned)blocks, 32 * WARPS, smem_t, s>>>(data, outer, m, inner, F.fac,
-                                                                                    mode, omega, xacc);
+                                                                                    F.kc, mode, omega, xacc);
   return true;
 }
 

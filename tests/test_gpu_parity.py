@@ -30,8 +30,8 @@ PARAMS = dict(nu=0.3, beta=0.05, lam=1.0)
 
 
 def default_mode(d):
-    """The library's default auxiliary combination (reading R8'): additive in 3D."""
-    return "add" if d == 3 else "mult"
+    """The library's default auxiliary combination (reading R8'): additive."""
+    return "add"
 
 
 def b0_for(d):
@@ -256,8 +256,8 @@ def test_aux_preconditioner_matches_oracle(case):
         disc = Discretization(case.d, case.p, case.n)
         A = disc.assemble(case.form)
         B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels)
-        # default: multiplicative in 2D, additive in 3D (reading R8'); test the multiplicative here
-        assert ig.igacd_get_preconditioner(h) == (ig.IGACD_PRECOND_AUX if case.d == 2 else ig.IGACD_PRECOND_AUX_ADD)
+        # default: additive (reading R8'); test the multiplicative combination here
+        assert ig.igacd_get_preconditioner(h) == ig.IGACD_PRECOND_AUX_ADD
         ig.igacd_set_preconditioner(h, ig.IGACD_PRECOND_AUX)
         assert ig.igacd_aux_is_exact(h) == int(B.exact)
         if not B.exact:
