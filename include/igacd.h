@@ -82,6 +82,11 @@ int igacd_residual(igacd_handle h, int level, const double* b, const double* x, 
 int igacd_smooth(igacd_handle h, int level, const double* b, double* x, int sweeps, double omega, void* stream);
 
 /* x_coarse = P_level^T x_fine   (R3, restriction to level+1). */
+/* x = T_l^{-1} b on `level` for the vector system: the smoother's preconditioner
+ * T_n^p = I_d (x) T(m_{p-1}) (x) .. (x) T(m_{p-1}) (reading R4'), applied as
+ * banded Cholesky line solves along each direction.  b, x: device, d*m^d doubles, no aliasing. */
+int igacd_tsolve(igacd_handle h, int level, const double* b, double* x, void* stream);
+
 int igacd_restrict(igacd_handle h, int level, const double* x_fine, double* x_coarse, void* stream);
 
 /* x_fine = P_level x_coarse (accumulate == 0) or x_fine += P_level x_coarse (accumulate != 0). */

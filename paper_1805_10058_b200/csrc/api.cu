@@ -375,14 +375,13 @@ static void smooth(Handle& h, int sy, int l, const double* b, double*& cur, doub
   Epi ep{};
   ep.b = b;
   for (int k = 0; k < sweeps; ++k) {
-    if (k == 0 && from_zero) {
-      launch_copy(h, b, L.r, L.ndof, s);
-      launch_zero(h, cur, L.ndof, s);
-    } else {
-      launch_operator(h, sy, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
-    }
-    for (int a = 0; a + 1 < h.dim; ++a) launch_band_solve(h, h.sys[sy].nc, l, a, h.lv[l].T, L.r, 0, 0.0, nullptr, s);
-    launch_band_solve(h, h.sys[sy].nc, l, h.dim - 1, h.lv[l].T, L.r, 1, L.omega_t, cur, s);
+    // from x = 0 the residual is b: the first line solve reads b and the last one assigns
+    // x = omega_t T^{-1} b (no copy of b, no zeroing of x)
+    const bool first = k == 0 && from_zero;
+    if (!first) launch_operator(h, sy, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
+    for (int a = 0; a + 1 < h.dim; ++a)
+      launch_band_solve(h, h.sys[sy].nc, l, a, h.lv[l].T, L.r, 0, 0.0, nullptr, s, (first && a == 0) ? b : nullptr);
+    launch_band_solve(h, h.sys[sy].nc, l, h.dim - 1, h.lv[l].T, L.r, first ? 2 : 1, L.omega_t, cur, s);
   }
 }
 
@@ -418,8 +417,7 @@ static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, c
 static void aux_solve(Handle& h, const double* sb, double* sx, cudaStream_t s) {
   System& A = h.sys[1];
   if (A.tensor_exact) {
-    launch_copy(h, sb, sx, A.lv[0].ndof, s);
-    for (int a = 0; a < h.dim; ++a) launch_band_solve(h, 1, 0, a, A.tf[a], sx, 0, 0.0, nullptr, s);
+    for (int a = 0; a < h.dim; ++a) launch_band_solve(h, 1, 0, a, A.tf[a], sx, 0, 0.0, nullptr, s, a == 0 ? sb : nullptr);
     return;
   }
   vcycle_level(h, 1, 0, sb, sx, s);
@@ -868,6 +866,19 @@ int igacd_smooth(igacd_handle h, int level, const double* b, double* x, int swee
   double* oth = L.t;
   jacobi_sweeps(*hh, 0, level, b, cur, oth, sweeps, w, (cudaStream_t)stream);
   if (cur != x) launch_copy(*hh, cur, x, L.ndof, (cudaStream_t)stream);
+  API_END
+}
+
+int igacd_tsolve(igacd_handle h, int level, const double* b, double* x, void* stream) {
+  API_BEGIN
+  Handle* hh = H(h);
+  check_level(hh, level);
+  check_ptr(b);
+  check_ptr(x);
+  if (b == x) throw Error{IGACD_E_ARG, "b and x must not alias"};
+  const Level& L = hh->lv[level];
+  for (int a = 0; a < hh->dim; ++a)
+    launch_band_solve(*hh, hh->dim, level, a, L.T, x, 0, 0.0, nullptr, (cudaStream_t)stream, a == 0 ? b : nullptr);
   API_END
 }
 

@@ -226,8 +226,11 @@ void launch_scal(Handle& h, double* a, double f, size_t n, cudaStream_t s);
 
 // ---- linesolve.cu -------------------------------------------------------------------
 void band_cholesky(const std::vector<double>& F, int m, int w, std::vector<double>& Lb, std::vector<double>& inv);
+// data <- F^{-1} src along `axis` (src = nullptr: in place).  mode 0: result in data;
+// mode 1: xacc += omega * result; mode 2: xacc = omega * result (data then holds the
+// forward-substitution intermediate in modes 1, 2)
 void launch_band_solve(Handle& h, int nc, int level, int axis, const BandFactor& F, double* data, int mode,
-                       double omega, double* xacc, cudaStream_t s);
+                       double omega, double* xacc, cudaStream_t s, const double* src = nullptr);
 
 // ---- common -------------------------------------------------------------------------
 inline void count_launch(Handle& h) { h.launches++; }

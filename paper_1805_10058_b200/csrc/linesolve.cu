@@ -11,6 +11,7 @@
 // memory.  Lines along the fastest axis are contiguous per thread (L1 absorbs the stride).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -83,22 +84,23 @@ __device__ __forceinline__ void ls_cp_async8(double* smem_dst, const double* gsr
 // the same numbers for every t, so they are held in registers (no shared-memory operand
 // loads) and the entering rows are read 8 steps ahead; the first / last rows use the tables.
 template <int W, int TP, bool FWD>
-__device__ __forceinline__ void band_sweep(double* tile, const double* __restrict__ G, const double* sI, int m,
-                                           int kc) {
+__device__ __forceinline__ void band_sweep(double* tile, const double* __restrict__ G, const double* __restrict__ gI,
+                                           int m, int kc) {
   auto row = [&](int t) { return FWD ? t : m - 1 - t; };
+  auto sIv = [&](int r) { return (r >= 0 && r < m) ? __ldg(gI + r) : 0.0; };   // 1/L[r][r], 0 outside
   if constexpr (W == 0) {
-    for (int t = 0; t < m; ++t) tile[t * TP] *= sI[t];
+    for (int t = 0; t < m; ++t) tile[t * TP] *= __ldg(gI + t);
   } else {
     double acc[W];
 #pragma unroll
-    for (int q = 0; q < W; ++q) acc[q] = tile[row(q) * TP] * sI[row(q)];
+    for (int q = 0; q < W; ++q) acc[q] = tile[row(q) * TP] * sIv(row(q));
     auto generic = [&](int t0, int t1) {
       for (int t = t0; t < t1; ++t) {
         const double v = acc[0];
-        const double enter = tile[row(t + W) * TP] * sI[row(t + W)];
+        const double enter = tile[row(t + W) * TP] * sIv(row(t + W));
 #pragma unroll
-        for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-G[t * (W + 1) + q], v, acc[q + 1]);
-        acc[W - 1] = fma(-G[t * (W + 1) + W - 1], v, enter);
+        for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-__ldg(G + t * (W + 1) + q), v, acc[q + 1]);
+        acc[W - 1] = fma(-__ldg(G + t * (W + 1) + W - 1), v, enter);
         tile[row(t) * TP] = v;
       }
     };
@@ -111,8 +113,8 @@ __device__ __forceinline__ void band_sweep(double* tile, const double* __restric
     generic(0, ta);
     double gc[W];
 #pragma unroll
-    for (int q = 0; q < W; ++q) gc[q] = G[ta * (W + 1) + q];
-    const double ic = sI[row(ta + W)];
+    for (int q = 0; q < W; ++q) gc[q] = __ldg(G + ta * (W + 1) + q);
+    const double ic = sIv(row(ta + W));
     constexpr int U = 8;
     int t = ta;
     for (; t + U <= tb; t += U) {
@@ -150,27 +152,22 @@ template <int W, int WARPS, int TW, int NBUF>
 __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restrict__ data, long long outer, int m,
                                                                long long inner, const double* __restrict__ fac,
                                                                int kc, int mode, double omega,
-                                                               double* __restrict__ xacc) {
+                                                               double* __restrict__ xacc, const double* src_arr) {
   extern __shared__ __align__(16) double sh[];
-  double* sF = sh;                          // [m][W+1]: forward column table (BandFactor::fac)
-  double* sB = sF + (size_t)m * (W + 1);    // [m][W+1]: backward column table
-  double* sI = sB + (size_t)m * (W + 1) + W;   // [-W, m+W): 1/L[k][k], zero outside [0, m)
+  // factor tables stay in global memory (L1-resident; only the first / last rows of a sweep
+  // read them, BandFactor::kc), so shared memory holds line tiles only
+  const double* __restrict__ gF = fac;                          // [m][W+1] forward column table
+  const double* __restrict__ gB = fac + (size_t)m * (W + 1);    // [m][W+1] backward column table
+  const double* __restrict__ gI = gB + (size_t)m * (W + 1);     // [m] 1/L[k][k]
   constexpr int TP = TW + 1;                // padded tile row (bank-conflict free for TW = 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int MP = m + 2 * W;                 // tile rows incl. W zero rows on each side
-  double* tiles = sI + m + W + (size_t)warp * NBUF * MP * TP + W * TP;   // buffer b: tiles + b*MP*TP
-  // the factor (precomputed [sF | sB | sI], BandFactor::fac) arrives in one batch of async copies
-  const int flen = 2 * (W + 1) * m;
-  for (int i = threadIdx.x; i < flen; i += blockDim.x) ls_cp_async8(sh + i, fac + i);
-  for (int i = threadIdx.x; i < m; i += blockDim.x) ls_cp_async8(sI + i, fac + flen + i);
-  for (int i = threadIdx.x; i < W; i += blockDim.x) sI[-1 - i] = sI[m + i] = 0.0;
+  double* tiles = sh + (size_t)warp * NBUF * MP * TP + W * TP;   // buffer b: tiles + b*MP*TP
   for (int b = 0; b < NBUF; ++b) {
     double* t = tiles + (size_t)b * MP * TP;
     for (int i = lane; i < W * TP; i += 32) t[-W * TP + i] = t[m * TP + i] = 0.0;
   }
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
+  __syncwarp();
   const long long lines = outer * inner;
   const long long groups = (lines + TW - 1) / TW;
   const long long stride = (long long)gridDim.x * WARPS;
@@ -179,7 +176,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
     const long long l0 = g * TW;
     const int nl = (int)min((long long)TW, lines - l0);
     if (inner == 1) {
-      const double* src = data + l0 * m;
+      const double* src = src_arr + l0 * m;
       int k = lane % m, ln = lane / m;   // e = ln * m + k, advanced by 32 without divisions
       for (int e = lane; e < nl * m; e += 32) {
         ls_cp_async8(&tile[k * TP + ln], src + e);
@@ -188,7 +185,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
       }
     } else {   // lanes = consecutive lines: coalesced except where the group crosses an `outer` step
       const long long l = l0 + lane;
-      const double* src = data + (l / inner) * (long long)m * inner + (l % inner);
+      const double* src = src_arr + (l / inner) * (long long)m * inner + (l % inner);
       double* tp = tile + lane;
       if (lane < nl)
 #pragma unroll 4
@@ -215,7 +212,22 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
     const long long l0 = g * TW;
     const int nl = (int)min((long long)TW, lines - l0);
     constexpr int U = 16;
-    if (inner == 1 && mode != 0) {
+    if (inner == 1 && mode == 2) {
+      double* dst = xacc + l0 * m;
+      const int tot = nl * m;
+      int k = lane % m, ln = lane / m;
+      for (int e0 = lane; e0 < tot; e0 += 32 * U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + 32 * u;
+          if (e < tot) {
+            dst[e] = omega * tile[k * TP + ln];
+            k += 32;
+            while (k >= m) { k -= m; ++ln; }
+          }
+        }
+      }
+    } else if (inner == 1 && mode != 0) {
       double* dst = xacc + l0 * m;
       const int tot = nl * m;
       int k = lane % m, ln = lane / m;
@@ -257,10 +269,11 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
       double* dst = (mode == 0 ? data : xacc) + (l / inner) * (long long)m * inner + (l % inner);
       const double* tp = tile + lane;
       if (lane < nl) {
-        if (mode == 0) {
+        if (mode == 0 || mode == 2) {
+          const double f = mode == 0 ? 1.0 : omega;
 #pragma unroll 4
           for (int k = 0; k < m; ++k) {
-            *dst = *tp;
+            *dst = f * *tp;
             tp += TP;
             dst += inner;
           }
@@ -300,12 +313,12 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
     }
     __syncwarp();
     const int nl = (int)min((long long)TW, lines - g * TW);
-    if (inner == 1 && mode != 0) acc_load(xacc + g * TW * m, lane, nl * m, xa0);   // batch 0, ahead
+    if (inner == 1 && mode == 1) acc_load(xacc + g * TW * m, lane, nl * m, xa0);   // batch 0, ahead
     if (lane < nl) {
       // forward  y_k = i_k b_k - sum_j (i_k L[k][k-j]) y_{k-j}
       // backward x_k = i_k y_k - sum_j (i_k L[k+j][k]) x_{k+j}
-      band_sweep<W, TP, true>(tile + lane, sF, sI, m, kc);
-      band_sweep<W, TP, false>(tile + lane, sB, sI, m, kc);
+      band_sweep<W, TP, true>(tile + lane, gF, gI, m, kc);
+      band_sweep<W, TP, false>(tile + lane, gB, gI, m, kc);
     }
     __syncwarp();
     store(g, tile);
@@ -390,9 +403,8 @@ static int num_sms() {
 
 template <int W, int WARPS, int TW, int NBUF>
 static bool try_tiled(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode,
-                      double omega, double* xacc, cudaStream_t s) {
-  const size_t smem_t = sizeof(double) * (2 * (size_t)m * (W + 1) + m + 2 * W +
-                                          (size_t)WARPS * NBUF * (m + 2 * W) * (TW + 1));
+                      double omega, double* xacc, const double* src, cudaStream_t s) {
+  const size_t smem_t = sizeof(double) * ((size_t)WARPS * NBUF * (m + 2 * W) * (TW + 1));
   if (smem_t > 200 * 1024) return false;
   static size_t attr_t = 0;
   if (smem_t > 48 * 1024 && attr_t < smem_t) {
@@ -413,7 +425,7 @@ static bool try_tiled(double* data, long long outer, int m, long long inner, con
   }
   blocks = std::min<long long>(blocks, (long long)occ * num_sms());
   k_band_solve_tiled<W, WARPS, TW, NBUF><<<(unsigned)blocks, 32 * WARPS, smem_t, s>>>(data, outer, m, inner, F.fac,
-                                                                                    F.kc, mode, omega, xacc);
+                                                                                    F.kc, mode, omega, xacc, src);
   return true;
 }
 
@@ -428,15 +440,26 @@ static int band_nbuf() {
   return v;
 }
 
+static int band_warps() {   // IGACD_BAND_WARPS: warps per CTA of the tiled line solve (1 default, 2)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IGACD_BAND_WARPS");
+    v = (e && e[0] == '2') ? 2 : 1;
+  }
+  return v;
+}
+
 template <int W>
 static void launch_w(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode,
-                     double omega, double* xacc, cudaStream_t s) {
+                     double omega, double* xacc, const double* src, cudaStream_t s) {
   // double-buffered 32-line tiles (2 warps) when they fit, else the widest single-buffered tile
-  if (band_nbuf() == 2 && try_tiled<W, 2, 32, 2>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
-  if (try_tiled<W, 2, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
-  if (try_tiled<W, 1, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
-  if (try_tiled<W, 1, 16, 1>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
-  if (try_tiled<W, 1, 8, 1>(data, outer, m, inner, F, mode, omega, xacc, s)) return;
+  if (band_nbuf() == 2 && try_tiled<W, 2, 32, 2>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
+  // one warp per CTA packs 5 tiles per SM for m = 162 (2 warps per CTA: 4)
+  if (band_warps() == 1 && try_tiled<W, 1, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
+  if (try_tiled<W, 2, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
+  if (try_tiled<W, 1, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
+  if (try_tiled<W, 1, 16, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
+  if (try_tiled<W, 1, 8, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
   const size_t smem = sizeof(double) * ((size_t)m * (W + 1) + m);
   static int attr_set = 0;
   if (smem > 48 * 1024 && attr_set < (int)smem) {
@@ -448,25 +471,30 @@ static void launch_w(double* data, long long outer, int m, long long inner, cons
   long long blocks = (lines + bs - 1) / bs;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
-  k_band_solve<W><<<(unsigned)blocks, bs, smem, s>>>(data, outer, m, inner, F.Lb, F.inv, mode, omega, xacc);
+  // the in-place fallback: stage src into data, and mode 2 (assign) as accumulate into zeros
+  if (src != data) IGACD_CUDA(cudaMemcpyAsync(data, src, sizeof(double) * lines * m, cudaMemcpyDeviceToDevice, s));
+  if (mode == 2) IGACD_CUDA(cudaMemsetAsync(xacc, 0, sizeof(double) * lines * m, s));
+  k_band_solve<W><<<(unsigned)blocks, bs, smem, s>>>(data, outer, m, inner, F.Lb, F.inv, mode == 0 ? 0 : 1, omega,
+                                                     xacc);
 }
 
 // data <- F^{-1} data along axis `axis` of a [nc][m]^dim array; mode 1: xacc += omega * F^{-1} data
 // (data is then left holding the forward-substitution intermediate).
 void launch_band_solve(Handle& h, int nc, int level, int axis, const BandFactor& F, double* data, int mode,
-                       double omega, double* xacc, cudaStream_t s) {
+                       double omega, double* xacc, cudaStream_t s, const double* src) {
   const long long m = h.lv[level].m;
+  if (!src) src = data;
   long long outer = nc, inner = 1;
   for (int a = 0; a < axis; ++a) outer *= m;
   for (int a = axis + 1; a < h.dim; ++a) inner *= m;
   switch (F.w) {
-    case 0: launch_w<0>(data, outer, (int)m, inner, F, mode, omega, xacc, s); break;
-    case 1: launch_w<1>(data, outer, (int)m, inner, F, mode, omega, xacc, s); break;
-    case 2: launch_w<2>(data, outer, (int)m, inner, F, mode, omega, xacc, s); break;
-    case 3: launch_w<3>(data, outer, (int)m, inner, F, mode, omega, xacc, s); break;
-    case 4: launch_w<4>(data, outer, (int)m, inner, F, mode, omega, xacc, s); break;
-    case 5: launch_w<5>(data, outer, (int)m, inner, F, mode, omega, xacc, s); break;
-    case 6: launch_w<6>(data, outer, (int)m, inner, F, mode, omega, xacc, s); break;
+    case 0: launch_w<0>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
+    case 1: launch_w<1>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
+    case 2: launch_w<2>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
+    case 3: launch_w<3>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
+    case 4: launch_w<4>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
+    case 5: launch_w<5>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
+    case 6: launch_w<6>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
     default: throw Error{IGACD_E_ARG, "band width out of range"};
   }
   IGACD_LAUNCH_CHECK();

@@ -54,6 +54,7 @@ _aux_exact = _sig("igacd_aux_is_exact", [_vp, _P(_c_int)])
 _apply_aux = _sig("igacd_apply_aux", [_vp, _c_int, _vp, _vp, _vp])
 _aux_omega = _sig("igacd_aux_omega", [_vp, _c_int, _P(_c_double), _P(_c_double)])
 _solve = _sig("igacd_solve", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
+_tsolve = _sig("igacd_tsolve", [_vp, _c_int, _vp, _vp, _vp])
 _set_aux_sweeps = _sig("igacd_set_aux_sweeps", [_vp, _c_int, _c_int])
 _set_graphs = _sig("igacd_set_graphs", [_vp, _c_int])
 _gmres = _sig("igacd_gmres", [_vp, _vp, _vp, _c_double, _c_int, _c_int, _P(_c_int), _P(_c_double), _vp])
@@ -226,6 +227,10 @@ def igacd_solve(h, b, x, tol, maxit, stream=None, raise_on_noconv=True):
     if rc != IGACD_E_NOCONV or raise_on_noconv:
         _check(rc)
     return it.value, rel.value
+
+
+def igacd_tsolve(h, level, b, x, stream=None):
+    _check(_tsolve(h, level, _dptr(b), _dptr(x), _stream(stream)))
 
 
 def igacd_set_aux_sweeps(h, nu_pre, nu_post):

@@ -463,3 +463,21 @@ def test_graph_replay_is_bit_identical_to_eager_launches():
         assert torch.equal(xg, xe)
     finally:
         ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("case", [Case(2, 3, 40, levels=2), Case(2, 6, 30, levels=2), Case(3, 4, 10, levels=2),
+                                  Case(3, 2, 14, levels=2), Case(2, 1, 12, levels=2)], ids=repr)
+def test_tsolve_matches_oracle(case):
+    """Line solves alone: x = T^{-1} b (I_d (x) T(m_{p-1}) (x) ..) vs the oracle's sparse LU."""
+    h = case.handle()
+    try:
+        A = Discretization(case.d, case.p, case.n).assemble(case.form)
+        H = Hierarchy(A, case.d, case.p, case.n, case.levels)
+        for l in range(len(H.ns) - 1):
+            N = H.A[l].shape[0]
+            b = np.random.default_rng(30 + l).standard_normal(N)
+            x = torch.zeros(N, dtype=torch.float64, device="cuda")
+            ig.igacd_tsolve(h, l, to_dev(b), x)
+            assert_close(to_host(x), H.Tlu[l].solve(b), 1e-12, "T^-1 level %d" % l)
+    finally:
+        ig.igacd_destroy(h)
