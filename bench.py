@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--apply-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true")
     return ap.parse_args()
 
 
@@ -157,6 +158,21 @@ def run_reference(args, cfg, rank, world):
 BASE_METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 
 
+def rank_rhs(cfg, rank):
+    """Replicas: rank r solves its own seeded right-hand side (seed + r)."""
+    return inputs.rhs(cfg, seed=cfg.seed + rank)
+
+
+def max_over_ranks(value, dist, device):
+    """Max of a per-rank time over all ranks (the slowest replica sets the job time)."""
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -181,7 +197,7 @@ def main():
     stream = torch.cuda.current_stream()
     h = ig.igacd_create(cfg.dim, cfg.p, cfg.n, cfg.nu, cfg.beta, cfg.lam, cfg.b0, levels=cfg.levels)
     N = ig.igacd_ndof(h)
-    b_host = inputs.rhs(cfg, seed=cfg.seed + rank)
+    b_host = rank_rhs(cfg, rank)
     b = torch.from_numpy(b_host).cuda()
     x = torch.zeros_like(b)
     pk, pk_src = peaks()
@@ -210,10 +226,7 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     launches, apply_launches, apply_ms = ig.igacd_get_profile(h)
     ig.igacd_set_profiling(h, False)
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, dist, "cuda")
     value = N * world / (ms / 1000.0)
 
     # roofline of the dominant kernel (level-0 operator apply inside the timed solves)
@@ -224,6 +237,26 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "apply_traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(cfg.name)
+
+    # the apply is FP64-issue-bound: algorithmic FP64
+    # instructions per unknown of the sum-factorised operator with symmetric pairing,
+    # 3D: (66p + 90)/3, 2D: (22p + 26)/2; peak = measured DFMA issue rate
+    fp64_per_unknown = (66 * cfg.p + 90) / 3.0 if cfg.dim == 3 else (22 * cfg.p + 26) / 2.0
+    fp64_peak = 17.1e12   # tools/microbench/fp64_peak.cu on B200 (59 DFMA/clk/SM at 1.965 GHz)
+    fp64_achieved = fp64_per_unknown * N / (apply_avg_ms * 1e-3)
+
+    # ---- GMRES (the paper's PGMRES) on the same system: one solve ---------------------------
+    gmres = None
+    if not args.no_gmres:
+        xg = torch.zeros_like(b)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        git, grel = ig.igacd_gmres(h, b, xg, cfg.tol, args.maxit, restart=30, raise_on_noconv=False)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gmres = {"restart": 30, "iterations": git, "relres": grel,
+                 "time_to_solution_s": g0.elapsed_time(g1) / 1000.0}
+        del xg
 
     # ---- operator-apply sweep (rotating buffers > L2) -----------------------------------
     nbuf = max(2, int(np.ceil(2 * L2_BYTES / (16 * N))) + 1)
@@ -256,10 +289,7 @@ def main():
         h1.record(stream)
         torch.cuda.synchronize()
         ems = h0.elapsed_time(h1) / args.steps
-        if dist is not None:
-            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(ems, dist, "cuda")
         e2e = {"value": N * world / (ems / 1000.0), "unit": "DOF/s", "h2d_bytes_per_step": 8 * N,
                "d2h_bytes_per_step": 8 * N, "ms_per_step": ems}
 
@@ -279,6 +309,7 @@ def main():
                        "l2": "solve vectors exceed L2 (3D) / apply sweep rotates %d buffer pairs > 2xL2" % nbuf,
                        "parallelism": "replicas" if world > 1 else "single"},
             "time_to_solution_s": ms / 1000.0, "pcg_iterations": its[-1], "relres": rel,
+            "preconditioner": "aux-additive (R8') + V-cycle (Toeplitz smoother R4')",
             "apply": {"dof_per_s": N / (sweep_ms * 1e-3), "ms": sweep_ms,
                       "gbs": 16 * N / (sweep_ms * 1e-3) / 1e9,
                       "hbm_frac": 16 * N / (sweep_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
@@ -286,6 +317,10 @@ def main():
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk_src,
                          "kernel": "k_op%dd<p=%d> (level-0 apply inside PCG)" % (cfg.dim, cfg.p),
                          "launches": apply_launches, "avg_ms": apply_avg_ms},
+            "roofline_fp64": {"bound": "alu", "achieved": fp64_achieved / 1e12, "peak": fp64_peak / 1e12,
+                              "unit": "T FP64 instr/s", "frac": fp64_achieved / fp64_peak,
+                              "per_unknown": fp64_per_unknown, "peak_source": "measured (tools/microbench)"},
+            "gmres": gmres,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
