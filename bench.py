@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="bracket the first timed step with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     return ap.parse_args()
 
 
@@ -217,8 +219,12 @@ def main():
     with Clocks(local) as clk:
         e0.record(stream)
         its = []
-        for _ in range(args.steps):
+        for k in range(args.steps):
+            if args.profile_step and k == 0:
+                torch.cuda.profiler.start()
             it, rel = ig.igacd_solve(h, b, x, cfg.tol, args.maxit, raise_on_noconv=False)
+            if args.profile_step and k == 0:
+                torch.cuda.profiler.stop()
             its.append(it)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -315,7 +321,8 @@ def main():
                       "hbm_frac": 16 * N / (sweep_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk_src,
-                         "kernel": "k_op%dd<p=%d> (level-0 apply inside PCG)" % (cfg.dim, cfg.p),
+                         "kernel": ("k_slab3d + k_col3d<p=%d> (level-0 apply inside PCG)" % cfg.p if cfg.dim == 3
+                                    else "k_op2d<p=%d> (level-0 apply inside PCG)" % cfg.p),
                          "launches": apply_launches, "avg_ms": apply_avg_ms},
             "roofline_fp64": {"bound": "alu", "achieved": fp64_achieved / 1e12, "peak": fp64_peak / 1e12,
                               "unit": "T FP64 instr/s", "frac": fp64_achieved / fp64_peak,

@@ -466,9 +466,11 @@ def test_graph_replay_is_bit_identical_to_eager_launches():
 
 
 @pytest.mark.parametrize("case", [Case(2, 3, 40, levels=2), Case(2, 6, 30, levels=2), Case(3, 4, 10, levels=2),
-                                  Case(3, 2, 14, levels=2), Case(2, 1, 12, levels=2)], ids=repr)
+                                  Case(3, 2, 14, levels=2), Case(2, 1, 12, levels=2), Case(3, 3, 20, levels=2),
+                                  Case(2, 5, 60, levels=2)], ids=repr)
 def test_tsolve_matches_oracle(case):
-    """Line solves alone: x = T^{-1} b (I_d (x) T(m_{p-1}) (x) ..) vs the oracle's sparse LU."""
+    """Line solves alone: x = T^{-1} b (I_d (x) T(m_{p-1}) (x) ..) vs the oracle's sparse LU.
+    Levels with m >= 4p use the two-partition (SPIKE) kernel, odd m gives unequal halves."""
     h = case.handle()
     try:
         A = Discretization(case.d, case.p, case.n).assemble(case.form)
