@@ -282,11 +282,14 @@ __global__ void __launch_bounds__(T2* T3, MINB) k_op3d(const OpParams op, const 
       }
     }
   }
-  // stage A work item: (half of the tile rows, component, halo column), lanes along columns;
-  // each item marches down its T2/2 output rows with a register window of T2/2 + 2P inputs
-  constexpr int RH = T2 / 2;
-  static_assert(T2 % 2 == 0, "two row halves");
-  constexpr int NITEMS = 2 * NC * HC;
+  // stage A work item: (row segment, component, halo column), lanes along columns; each
+  // item marches down its RH = T2/RS output rows with a register window of RH + 2P inputs.
+  // The scalar system splits the rows in 4 (160 items for 256 threads instead of 80: the
+  // barrier after stage A was the top stall), the vector system in 2.
+  constexpr int RS = NC == 1 ? 4 : 2;
+  constexpr int RH = T2 / RS;
+  static_assert(T2 % RS == 0, "row segments");
+  constexpr int NITEMS = RS * NC * HC;
   const bool wzb = __any_sync(0xffffffffu, zoneB);
   const int bo = tr * HC + tc + P;     // stage-B window centre
   const int pto = gr * m + gc;         // in-slab output offset
