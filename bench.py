@@ -113,7 +113,7 @@ def cpu_sample(cfg):
     from oracle.multigrid import AuxPreconditioner
     from oracle.operator import Discretization, form_alfven
     n = 6 if cfg.dim == 3 else 32
-    small = cfg.with_(n=n, levels=0)
+    small = cfg.with_(n=n, levels=2)   # two levels: a V-cycle, like the GPU solve (R6 would stop at one)
     if small not in _CPU_CACHE:
         A = Discretization(small.dim, small.p, small.n).assemble(form_alfven(small.nu, small.beta, small.lam, small.b0))
         mode = "add"   # the library default (reading R8')
@@ -123,7 +123,7 @@ def cpu_sample(cfg):
     t0 = time.perf_counter()
     _, it, hist = pcg(A, b, B, small.tol, 5000)
     dt = time.perf_counter() - t0
-    desc = ("oracle PCG + aux/V-cycle solve (setup untimed) of %s with n=%d (%d DOFs, %d iterations, "
+    desc = ("oracle PCG + aux/2-level V-cycle solve (setup untimed) of %s with n=%d (%d DOFs, %d iterations, "
             "rel.res %.1e)" % (cfg.name, n, small.ndof, it, hist[-1]))
     return small.ndof / dt, dt, desc
 

@@ -17,7 +17,7 @@ Readings (DESIGN.md):
       after K=30 normalised steps v <- T^{-1} A v / ||.||_2 from the same start vector.
   R5  coarsest level solved exactly (dense Cholesky, library primitive scipy cho_solve).
   R6  levels: n_{l+1} = n_l/2 while n_l is even, the next interior size n_l/2+p-2 >= 1 and
-      d*(n_l+p-2)^d > 1500 (or exactly ``levels`` levels when requested).
+      d*(n_l+p-2)^d > 6000 (or exactly ``levels`` levels when requested).
   R8  preconditioner: the V-cycle alone, or combined multiplicatively with a correction on the
       auxiliary space span{b0 s} (the kernel of the lambda-term curl(b0 x u), which is exactly
       representable: Pi s = b0 s maps the scalar spline space into V_h):
@@ -35,7 +35,7 @@ from inputs import hash_vector
 from .bspline import cardinal
 from .transfer import prolongation
 
-NCOARSE_MAX = 1500
+NCOARSE_MAX = 6000
 POWER_STEPS = 30
 
 

@@ -11,7 +11,7 @@
 namespace igacd {
 
 constexpr int MAXP = 6;   // highest supported B-spline degree
-constexpr int NCOARSE_MAX = 1500;  // reading R6: coarsen while d*m^d exceeds this
+constexpr int NCOARSE_MAX = 6000;  // reading R6: coarsen while d*m^d exceeds this
 constexpr int POWER_STEPS = 30;    // reading R4: power steps for rho(D^-1 A)
 constexpr size_t COARSE_DENSE_MAX = 8192;  // largest coarsest level given a dense inverse
 

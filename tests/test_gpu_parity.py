@@ -274,8 +274,9 @@ def test_aux_preconditioner_matches_oracle(case):
 
 SOLVE_CASES = [Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels=2),
                Case(2, 3, 32, nu=1.0, beta=0.1, levels=0), Case(3, 2, 8, nu=1.0, beta=0.1, levels=2),
-               Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)), Case(2, 5, 32, nu=1e-4, beta=1e-4, b0=(1.0, 0.0)),
-               Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0))]
+               Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)),
+               Case(2, 5, 32, nu=1e-4, beta=1e-4, b0=(1.0, 0.0), levels=3),
+               Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0), levels=2)]
 
 
 @pytest.mark.parametrize("case", SOLVE_CASES, ids=repr)
@@ -299,7 +300,7 @@ def test_solve_matches_oracle(case):
 
 
 def test_plain_vcycle_preconditioner_solve():
-    case = Case(2, 3, 32, nu=1.0, beta=0.1, levels=0)
+    case = Case(2, 3, 32, nu=1.0, beta=0.1, levels=3)
     h = case.handle()
     try:
         ig.igacd_set_preconditioner(h, ig.IGACD_PRECOND_VCYCLE)
@@ -383,7 +384,7 @@ GMRES_CASES = [(Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels
                (Case(3, 2, 8, nu=1.0, beta=0.1, levels=2), 30),
                (Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)), 30),
                (Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)), 7),
-               (Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0)), 5)]
+               (Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0), levels=2), 5)]
 
 
 @pytest.mark.parametrize("case,restart", GMRES_CASES, ids=lambda v: repr(v))
@@ -408,7 +409,7 @@ def test_gmres_matches_oracle(case, restart):
 
 
 @pytest.mark.parametrize("case", [Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)),
-                                  Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0))], ids=repr)
+                                  Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0), levels=2)], ids=repr)
 def test_additive_aux_preconditioner_and_solve(case):
     h = case.handle()
     try:
@@ -448,7 +449,7 @@ def test_gmres_zero_rhs_and_arguments():
 
 
 def test_graph_replay_is_bit_identical_to_eager_launches():
-    case = Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0))
+    case = Case(3, 3, 8, nu=1.0, beta=1e-2, b0=(0.0, 0.0, 1.0), levels=2)
     h = case.handle()
     try:
         N = ig.igacd_ndof(h)

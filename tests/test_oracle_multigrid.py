@@ -47,10 +47,10 @@ def test_galerkin_coarse_operator_equals_coarse_discretization(d, p, nc):
 
 def test_level_rule():
     assert level_sizes(2, 2, 16, 2) == [16, 8]
-    assert level_sizes(3, 4, 160) == [160, 80, 40, 20, 10, 5]
-    assert level_sizes(2, 3, 256) == [256, 128, 64, 32, 16]
-    assert level_sizes(3, 3, 64) == [64, 32, 16, 8, 4]
-    assert level_sizes(2, 5, 1024)[-1] == 16
+    assert level_sizes(3, 4, 160) == [160, 80, 40, 20, 10]
+    assert level_sizes(2, 3, 256) == [256, 128, 64, 32]
+    assert level_sizes(3, 3, 64) == [64, 32, 16, 8]
+    assert level_sizes(2, 5, 1024)[-1] == 32
 
 
 def _setup(d=2, p=2, n=8, levels=0, nu=1.0, beta=0.05, b0=(0.6, 0.8)):
