@@ -119,6 +119,9 @@ int igacd_get_preconditioner(igacd_handle h, int* mode);
 #define IGACD_SMOOTH_JACOBI 0
 #define IGACD_SMOOTH_TOEPLITZ 1
 int igacd_set_smoother(igacd_handle h, int kind);
+/* Smoother of the auxiliary scalar V-cycle: IGACD_SMOOTH_JACOBI, IGACD_SMOOTH_TOEPLITZ, or -1
+ * (default) for the same smoother as the vector V-cycle.  IGACD_E_ARG without an auxiliary space. */
+int igacd_set_aux_smoother(igacd_handle h, int kind);
 int igacd_get_smoother(igacd_handle h, int* kind);
 int igacd_aux_is_exact(igacd_handle h, int* exact);
 

@@ -155,7 +155,7 @@ class AuxPreconditioner:
     component (A_s is then one Kronecker product), else the V-cycle of A_s."""
 
     def __init__(self, A0, d, p, n, b0, levels=0, nu_pre=1, nu_post=1, smoother="toeplitz", mode="mult",
-                 aux_nu_pre=None, aux_nu_post=None):
+                 aux_nu_pre=None, aux_nu_post=None, aux_smoother=None):
         assert mode in ("mult", "add")
         aux_nu_pre = nu_pre if aux_nu_pre is None else aux_nu_pre
         aux_nu_post = nu_post if aux_nu_post is None else aux_nu_post
@@ -170,7 +170,7 @@ class AuxPreconditioner:
             self.Bs = self.lu.solve
         else:
             self.Vs = Hierarchy(As, d, p, n, levels, aux_nu_pre, aux_nu_post, ncomp=1, ns=self.V.ns,
-                                smoother=smoother)
+                                smoother=smoother if aux_smoother is None else aux_smoother)
             self.Bs = self.Vs.vcycle
 
     def __call__(self, r):

@@ -356,6 +356,10 @@ static void jacobi_sweeps(Handle& h, int sy, int l, const double* b, double*& cu
 // `sweeps` smoothing steps on x for A_l x = b (system sy).  from_zero: x is 0 on entry, so the
 // first step needs no operator apply.  JACOBI (R4): x <- x + omega D^{-1}(b - A x), ping-pong
 // buffers; TOEPLITZ (R4'): x <- x + omega_t T^{-1}(b - A x), T = T_n^p, in place.
+static int smoother_of(const Handle& h, int sy) {   // the auxiliary system may use its own
+  return (sy == 1 && h.aux_smoother >= 0) ? h.aux_smoother : h.smoother;
+}
+
 static void smooth(Handle& h, int sy, int l, const double* b, double*& cur, double*& oth, int sweeps, bool from_zero,
                    cudaStream_t s) {
   SysLevel& L = h.sys[sy].lv[l];
@@ -363,7 +367,7 @@ static void smooth(Handle& h, int sy, int l, const double* b, double*& cur, doub
     if (from_zero) launch_zero(h, cur, L.ndof, s);
     return;
   }
-  if (h.smoother == SMOOTH_JACOBI) {
+  if (smoother_of(h, sy) == SMOOTH_JACOBI) {
     int k = 0;
     if (from_zero) {
       launch_scale_dinv(h, sy, l, b, cur, L.omega, s);   // first sweep from x = 0: x = omega D^-1 b
@@ -398,7 +402,7 @@ static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, c
     return;
   }
   SysLevel& L = S.lv[l];
-  const int swaps = h.smoother == SMOOTH_JACOBI ? std::max(0, S.nu_pre - 1) + S.nu_post : 0;
+  const int swaps = smoother_of(h, sy) == SMOOTH_JACOBI ? std::max(0, S.nu_pre - 1) + S.nu_post : 0;
   double* cur = (swaps % 2 == 0) ? x : L.t;
   double* oth = (cur == x) ? L.t : x;
   smooth(h, sy, l, b, cur, oth, S.nu_pre, true, s);
@@ -960,6 +964,16 @@ int igacd_set_graphs(igacd_handle h, int enable) {
   API_END
 }
 
+int igacd_set_aux_smoother(igacd_handle h, int kind) {
+  API_BEGIN
+  Handle* hh = H(h);
+  if (!hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space on this handle"};
+  if (kind != -1 && kind != SMOOTH_JACOBI && kind != SMOOTH_TOEPLITZ) throw Error{IGACD_E_ARG, "unknown smoother"};
+  if (hh->aux_smoother != kind) graphs_reset(*hh);
+  hh->aux_smoother = kind;
+  API_END
+}
+
 int igacd_get_smoother(igacd_handle h, int* kind) {
   API_BEGIN
   check_ptr(kind);
@@ -1000,7 +1014,7 @@ int igacd_aux_omega(igacd_handle h, int level, double* omega, double* rho) {
   check_level(hh, level);
   if (!hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space on this handle"};
   const SysLevel& L = hh->sys[1].lv[level];
-  const bool t = hh->smoother == SMOOTH_TOEPLITZ;
+  const bool t = smoother_of(*hh, 1) == SMOOTH_TOEPLITZ;
   if (omega) *omega = t ? L.omega_t : L.omega;
   if (rho) *rho = t ? L.rho_t : L.rho;
   API_END

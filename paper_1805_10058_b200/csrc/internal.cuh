@@ -122,6 +122,7 @@ struct Handle {
   bool has_aux = false;
   int precond = PRECOND_VCYCLE;
   int smoother = SMOOTH_TOEPLITZ;
+  int aux_smoother = -1;        // smoother of the auxiliary V-cycle (-1: the same as `smoother`)
   // transfer scratch (max size), reductions
   double* scratch0 = nullptr;   // vector-system transfers
   double* scratch1 = nullptr;   // scalar-system transfers (the additive branch runs concurrently)

@@ -55,6 +55,7 @@ _apply_aux = _sig("igacd_apply_aux", [_vp, _c_int, _vp, _vp, _vp])
 _aux_omega = _sig("igacd_aux_omega", [_vp, _c_int, _P(_c_double), _P(_c_double)])
 _solve = _sig("igacd_solve", [_vp, _vp, _vp, _c_double, _c_int, _P(_c_int), _P(_c_double), _vp])
 _tsolve = _sig("igacd_tsolve", [_vp, _c_int, _vp, _vp, _vp])
+_set_aux_smoother = _sig("igacd_set_aux_smoother", [_vp, _c_int])
 _set_aux_sweeps = _sig("igacd_set_aux_sweeps", [_vp, _c_int, _c_int])
 _set_graphs = _sig("igacd_set_graphs", [_vp, _c_int])
 _gmres = _sig("igacd_gmres", [_vp, _vp, _vp, _c_double, _c_int, _c_int, _P(_c_int), _P(_c_double), _vp])
@@ -231,6 +232,10 @@ def igacd_solve(h, b, x, tol, maxit, stream=None, raise_on_noconv=True):
 
 def igacd_tsolve(h, level, b, x, stream=None):
     _check(_tsolve(h, level, _dptr(b), _dptr(x), _stream(stream)))
+
+
+def igacd_set_aux_smoother(h, kind):
+    _check(_set_aux_smoother(h, kind))
 
 
 def igacd_set_aux_sweeps(h, nu_pre, nu_post):
