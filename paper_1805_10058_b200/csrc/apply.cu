@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(NT) k_op2d(const OpParams op, const Epi ep, in
 // ---------------------------------------------------------------------------------------
 template <int P, int T2, int T3, int NC>
 struct Op3dShape {
-  static constexpr int NT = T2 * T3;
+  static constexpr int NT = (T2 * T3 + 31) / 32 * 32;   // full warps (T3 need not divide 32)
   static constexpr int R = 2 * P + 1;
   static constexpr int HR = T2 + 2 * P;
   static constexpr int HC = T3 + 2 * P;
@@ -240,7 +240,7 @@ struct Op3dShape {
 };
 
 template <int P, int T2, int T3, int NC, int MINB>
-__global__ void __launch_bounds__(T2* T3, MINB) k_op3d(const OpParams op, const Epi ep, int mode, int dot,
+__global__ void __launch_bounds__(Op3dShape<P, T2, T3, NC>::NT, MINB) k_op3d(const OpParams op, const Epi ep, int mode, int dot,
                                                     const double* __restrict__ x, double* __restrict__ y,
                                                     int chunk) {
   using Sh = Op3dShape<P, T2, T3, NC>;
@@ -256,10 +256,11 @@ __global__ void __launch_bounds__(T2* T3, MINB) k_op3d(const OpParams op, const 
   const int ms = m * m;                // ndof < 2^31 is checked on the host
   const int m3 = ms * m;
   const int tid = threadIdx.x;
-  const int tr = tid / T3, tc = tid % T3;
+  const bool real = tid < T2 * T3;   // padding threads of the last warp own no point
+  const int tr = real ? tid / T3 : T2 - 1, tc = real ? tid % T3 : 0;
   const int r0 = blockIdx.y * T2, q0 = blockIdx.x * T3;
   const int gr = r0 + tr, gc = q0 + tc;
-  const bool active = gr < m && gc < m;
+  const bool active = real && gr < m && gc < m;
   const bool zoneB = active && (gc < op.zoneL || gc >= op.zoneR);
   const int c0 = blockIdx.z * chunk;
   const int c1 = min(c0 + chunk, m);
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(T2* T3, MINB) k_op3d(const OpParams op, const 
 
 template <int P, int T2, int T3, int NC>
 struct SlabShape {
-  static constexpr int NT = T2 * T3;
+  static constexpr int NT = (T2 * T3 + 31) / 32 * 32;   // full warps (T3 need not divide 32)
   static constexpr int HR = T2 + 2 * P;
   static constexpr int HC = T3 + 2 * P;
   static constexpr int XS = HR * HC;
@@ -533,7 +534,7 @@ struct SlabShape {
 };
 
 template <int P, int T2, int T3, int NC>
-__global__ void __launch_bounds__(T2* T3) k_slab3d(const OpParams op, const double* __restrict__ x,
+__global__ void __launch_bounds__(SlabShape<P, T2, T3, NC>::NT) k_slab3d(const OpParams op, const double* __restrict__ x,
                                                    double* __restrict__ Z) {
   using Sh = SlabShape<P, T2, T3, NC>;
   constexpr int NT = Sh::NT, R = 2 * P + 1, HC = Sh::HC, XS = Sh::XS, US = Sh::US, LPT = Sh::LPT;
@@ -545,10 +546,11 @@ __global__ void __launch_bounds__(T2* T3) k_slab3d(const OpParams op, const doub
   const int ms = m * m, m3 = ms * m;
   const int s = blockIdx.z;
   const int tid = threadIdx.x;
-  const int tr = tid / T3, tc = tid % T3;
+  const bool real = tid < T2 * T3;   // padding threads of the last warp own no point
+  const int tr = real ? tid / T3 : T2 - 1, tc = real ? tid % T3 : 0;
   const int r0 = blockIdx.y * T2, q0 = blockIdx.x * T3;
   const int gr = r0 + tr, gc = q0 + tc;
-  const bool active = gr < m && gc < m;
+  const bool active = real && gr < m && gc < m;
   const bool zoneB = active && (gc < op.zoneL || gc >= op.zoneR);
   const bool wzb = __any_sync(0xffffffffu, zoneB);
   // ---- slab tile with halo -> shared memory (zero outside the domain)
@@ -807,7 +809,14 @@ __global__ void __launch_bounds__(256) k_col3d(const OpParams op, const Epi ep, 
 // launch configuration
 // ---------------------------------------------------------------------------------------
 constexpr int NT2D = 128;
-constexpr int T2_3D = 8, T3_3D = 32;      // k_op3d: one output point per thread
+constexpr int T2_3D = 8;                  // tile rows (direction 1) of the 3D kernels
+
+// tile columns (direction 2) of the 3D kernels: 32, or 27 when that wastes fewer columns
+// (m = 162: 6 x 27 = 162 exactly instead of 6 x 32 = 192)
+static int t3_for(int m) {
+  const int w32 = (m + 31) / 32 * 32, w27 = (m + 26) / 27 * 27;
+  return w27 < w32 ? 27 : 32;
+}
 constexpr int TARGET_CTAS = 4 * 148;
 
 // 3D vector system: slab kernel + column kernel (measured 1.4x faster than the fused
@@ -845,7 +854,8 @@ static Grid grid_for(const Handle& h, int level) {
     nch = (m + g.chunk - 1) / g.chunk;
     g.grid = dim3(tx, nch, 1);
   } else {
-    const int tx = (m + T3_3D - 1) / T3_3D, ty = (m + T2_3D - 1) / T2_3D;
+    const int T3 = t3_for(m);
+    const int tx = (m + T3 - 1) / T3, ty = (m + T2_3D - 1) / T2_3D;
     int nch = std::max(1, std::min(m, (TARGET_CTAS + tx * ty - 1) / (tx * ty)));
     g.chunk = (m + nch - 1) / nch;   // small levels: short chunks (latency), large: ~4 CTAs per SM
     g.chunk = std::max(g.chunk, std::min(m, 2));
@@ -869,20 +879,27 @@ int operator_ctas_sys(const Handle& h, int level, int nc) {
   return g.grid.x * g.grid.y * g.grid.z;
 }
 
-template <int P, int NC>
-static void launch_split3d(const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
-                           double* Z, cudaStream_t s) {
+template <int P, int NC, int T3>
+static void launch_split3d_t(const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                             double* Z, cudaStream_t s) {
   const int m = op.m;
-  using Sh = SlabShape<P, 8, 32, NC>;
+  using Sh = SlabShape<P, 8, T3, NC>;
   static bool attr = false;
   if (!attr) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_slab3d<P, 8, 32, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM));
+    IGACD_CUDA(cudaFuncSetAttribute(k_slab3d<P, 8, T3, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM));
     attr = true;
   }
-  k_slab3d<P, 8, 32, NC><<<dim3((m + 31) / 32, (m + 7) / 8, m), Sh::NT, Sh::SMEM, s>>>(op, x, Z);
+  k_slab3d<P, 8, T3, NC><<<dim3((m + T3 - 1) / T3, (m + 7) / 8, m), Sh::NT, Sh::SMEM, s>>>(op, x, Z);
   const int chunk = col_chunks(m);
   k_col3d<P, NC><<<dim3((m * m + 255) / 256, (m + chunk - 1) / chunk), 256, 0, s>>>(op, ep, mode, dot, Z, x, y,
                                                                                  chunk);
+}
+
+template <int P, int NC>
+static void launch_split3d(const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                           double* Z, cudaStream_t s) {
+  if (t3_for(op.m) == 27) launch_split3d_t<P, NC, 27>(op, ep, mode, dot, x, y, Z, s);
+  else launch_split3d_t<P, NC, 32>(op, ep, mode, dot, x, y, Z, s);
 }
 
 template <int P, int NC>
@@ -891,17 +908,24 @@ static void launch2d(const Grid& g, const OpParams& op, const Epi& ep, int mode,
   k_op2d<P, NT2D, NC><<<g.grid, NT2D, 0, s>>>(op, ep, mode, dot, x, y, g.chunk);
 }
 
-template <int P, int NC>
-static void launch3d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
-                     cudaStream_t s) {
-  using Sh = Op3dShape<P, T2_3D, T3_3D, NC>;
+template <int P, int NC, int T3>
+static void launch3d_t(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x,
+                       double* y, cudaStream_t s) {
+  using Sh = Op3dShape<P, T2_3D, T3, NC>;
   static bool attr = false;
   if (!attr) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_op3d<P, T2_3D, T3_3D, NC, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    IGACD_CUDA(cudaFuncSetAttribute(k_op3d<P, T2_3D, T3, NC, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     Sh::SMEM));
     attr = true;
   }
-  k_op3d<P, T2_3D, T3_3D, NC, 2><<<g.grid, Sh::NT, Sh::SMEM, s>>>(op, ep, mode, dot, x, y, g.chunk);
+  k_op3d<P, T2_3D, T3, NC, 2><<<g.grid, Sh::NT, Sh::SMEM, s>>>(op, ep, mode, dot, x, y, g.chunk);
+}
+
+template <int P, int NC>
+static void launch3d(const Grid& g, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                     cudaStream_t s) {
+  if (t3_for(op.m) == 27) launch3d_t<P, NC, 27>(g, op, ep, mode, dot, x, y, s);
+  else launch3d_t<P, NC, 32>(g, op, ep, mode, dot, x, y, s);
 }
 
 template <int P>

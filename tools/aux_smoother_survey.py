@@ -10,13 +10,16 @@ import torch  # noqa: E402
 import inputs  # noqa: E402
 from paper_1805_10058_b200 import igacd as ig  # noqa: E402
 
-for ci in [int(a) for a in sys.argv[1:]] or [1, 3, 4]:
+for ci in [int(a) for a in sys.argv[1:] if a != "--zero"] or [1, 3, 4]:
     c = inputs.config(ci)
     h = ig.igacd_create(c.dim, c.p, c.n, c.nu, c.beta, c.lam, c.b0, levels=c.levels)
     b = torch.from_numpy(inputs.rhs(c)).cuda()
     x = torch.zeros_like(b)
-    for aux in (-1, ig.IGACD_SMOOTH_JACOBI):
-        for sw in (1, 2):
+    combos = [(-1, 1), (-1, 0), (ig.IGACD_SMOOTH_JACOBI, 1), (ig.IGACD_SMOOTH_JACOBI, 2)]
+    if len(sys.argv) > 1 and sys.argv[1] == "--zero":
+        combos = [(-1, 1), (-1, 0)]
+    for aux, sw in combos:
+        if True:
             ig.igacd_set_aux_smoother(h, aux)
             ig.igacd_set_aux_sweeps(h, sw, sw)
             for rep in range(2):
