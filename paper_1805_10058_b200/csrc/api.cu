@@ -171,10 +171,33 @@ static void estimate_omega(Handle& h, int sy, int l, cudaStream_t s) {
   L.omega = 4.0 / (3.0 * 1.05 * L.rho);
 }
 
-// z <- T^{-1} z (in place) for system sy at level l: one band solve per direction
-static void apply_tinv(Handle& h, int sy, int l, double* z, cudaStream_t s) {
-  for (int a = 0; a < h.dim; ++a) launch_band_solve(h, h.sys[sy].nc, l, a, h.lv[l].T, z, 0, 0.0, nullptr, s);
+static bool band_slab_enabled() {   // IGACD_BAND_SLAB=0: one tiled pass per direction in 3D too
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IGACD_BAND_SLAB");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
+
+// data <- T_l^{-1} src (T = I_nc (x) T(m_{p-1})^{(x) d}, reading R4'), mode as launch_band_solve
+// (0: result in data; 1: xacc += omega * result; 2: xacc = omega * result).  3D: direction 0
+// by the tiled kernel, directions 1 and 2 together by the slab kernel when a slab fits.
+static void tinv(Handle& h, int sy, int l, const double* src, double* data, int mode, double omega, double* xacc,
+                 cudaStream_t s) {
+  const int nc = h.sys[sy].nc;
+  const BandFactor& T = h.lv[l].T;
+  if (h.dim == 3 && band_slab_enabled() && band_slab_fits(h.lv[l].m, T.w)) {
+    launch_band_solve(h, nc, l, 0, T, data, 0, 0.0, nullptr, s, src);
+    launch_band_solve_slab(h, nc, l, T, data, mode, omega, xacc, s);
+    return;
+  }
+  for (int a = 0; a + 1 < h.dim; ++a) launch_band_solve(h, nc, l, a, T, data, 0, 0.0, nullptr, s, a == 0 ? src : nullptr);
+  launch_band_solve(h, nc, l, h.dim - 1, T, data, mode, omega, xacc, s);
+}
+
+// z <- T^{-1} z (in place) for system sy at level l
+static void apply_tinv(Handle& h, int sy, int l, double* z, cudaStream_t s) { tinv(h, sy, l, z, z, 0, 0.0, nullptr, s); }
 
 // Reading R4': rho_t = ||T^{-1} A v|| after POWER_STEPS normalised steps v <- T^{-1} A v / ||.||
 // from the counter-based start vector; omega_t = 4 / (3 * 1.05 * rho_t).
@@ -383,9 +406,7 @@ static void smooth(Handle& h, int sy, int l, const double* b, double*& cur, doub
     // x = omega_t T^{-1} b (no copy of b, no zeroing of x)
     const bool first = k == 0 && from_zero;
     if (!first) launch_operator(h, sy, l, cur, L.r, EPI_RESID, DOT_NONE, ep, s);
-    for (int a = 0; a + 1 < h.dim; ++a)
-      launch_band_solve(h, h.sys[sy].nc, l, a, h.lv[l].T, L.r, 0, 0.0, nullptr, s, (first && a == 0) ? b : nullptr);
-    launch_band_solve(h, h.sys[sy].nc, l, h.dim - 1, h.lv[l].T, L.r, first ? 2 : 1, L.omega_t, cur, s);
+    tinv(h, sy, l, first ? b : L.r, L.r, first ? 2 : 1, L.omega_t, cur, s);
   }
 }
 
@@ -880,9 +901,7 @@ int igacd_tsolve(igacd_handle h, int level, const double* b, double* x, void* st
   check_ptr(b);
   check_ptr(x);
   if (b == x) throw Error{IGACD_E_ARG, "b and x must not alias"};
-  const Level& L = hh->lv[level];
-  for (int a = 0; a < hh->dim; ++a)
-    launch_band_solve(*hh, hh->dim, level, a, L.T, x, 0, 0.0, nullptr, (cudaStream_t)stream, a == 0 ? b : nullptr);
+  tinv(*hh, 0, level, b, x, 0, 0.0, nullptr, (cudaStream_t)stream);
   API_END
 }
 

@@ -232,6 +232,10 @@ void band_cholesky(const std::vector<double>& F, int m, int w, std::vector<doubl
 // forward-substitution intermediate in modes 1, 2)
 void launch_band_solve(Handle& h, int nc, int level, int axis, const BandFactor& F, double* data, int mode,
                        double omega, double* xacc, cudaStream_t s, const double* src = nullptr);
+// 3D: directions 1 and 2 of every [m][m] slab in one shared-memory pass (same modes)
+bool band_slab_fits(int m, int w);
+void launch_band_solve_slab(Handle& h, int nc, int level, const BandFactor& F, double* data, int mode, double omega,
+                            double* xacc, cudaStream_t s, const double* src = nullptr);
 
 // ---- common -------------------------------------------------------------------------
 inline void count_launch(Handle& h) { h.launches++; }

@@ -83,9 +83,9 @@ __device__ __forceinline__ void ls_cp_async8(double* smem_dst, const double* gsr
 // (BandFactor::kc): on the steps whose operands all come from those rows, G[t][q] and i_r are
 // the same numbers for every t, so they are held in registers (no shared-memory operand
 // loads) and the entering rows are read 8 steps ahead; the first / last rows use the tables.
-template <int W, int TP, bool FWD>
-__device__ __forceinline__ void band_sweep(double* tile, const double* __restrict__ G, const double* __restrict__ gI,
-                                           int m, int kc) {
+template <int W, bool FWD>
+__device__ __forceinline__ void band_sweep_s(double* tile, const int TP, const double* __restrict__ G,
+                                             const double* __restrict__ gI, int m, int kc) {
   auto row = [&](int t) { return FWD ? t : m - 1 - t; };
   auto sIv = [&](int r) { return (r >= 0 && r < m) ? __ldg(gI + r) : 0.0; };   // 1/L[r][r], 0 outside
   if constexpr (W == 0) {
@@ -140,6 +140,12 @@ __device__ __forceinline__ void band_sweep(double* tile, const double* __restric
     }
     generic(tb, m);
   }
+}
+
+template <int W, int TP, bool FWD>
+__device__ __forceinline__ void band_sweep(double* tile, const double* __restrict__ G, const double* __restrict__ gI,
+                                           int m, int kc) {
+  band_sweep_s<W, FWD>(tile, TP, G, gI, m, kc);
 }
 
 // Tiled variant: each warp stages TW lines in shared memory (coalesced loads/stores), and
@@ -478,6 +484,78 @@ static void launch_w(double* data, long long outer, int m, long long inner, cons
                                                      xacc);
 }
 
+
+// 3D, both in-slab axes in one pass: one CTA holds one [m][m] slab (directions 1, 2) of one
+// component in shared memory (row pitch m|1 odd: conflict-free row and column walks, W zero
+// rows before and after), solves every row (direction 2), then every column (direction 1),
+// one thread per line, and stores with the mode epilogue.  Versus two tiled passes: one
+// DRAM round trip instead of two.  The slab of (component c, index i0) is contiguous.
+template <int W>
+__global__ void __launch_bounds__(256) k_band_solve_slab(double* __restrict__ data, int m,
+                                                         const double* __restrict__ fac, int kc, int mode,
+                                                         double omega, double* __restrict__ xacc,
+                                                         const double* src_arr) {
+  extern __shared__ __align__(16) double sh[];
+  const int P = m | 1;
+  double* tile = sh + (size_t)W * P;
+  const double* __restrict__ gF = fac;
+  const double* __restrict__ gB = fac + (size_t)m * (W + 1);
+  const double* __restrict__ gI = gB + (size_t)m * (W + 1);
+  const size_t base = (size_t)blockIdx.x * m * m;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < W * P; i += nt) tile[-W * P + i] = tile[m * P + i] = 0.0;
+  if (P != m)
+    for (int i = tid; i < m; i += nt) tile[i * P + m] = 0.0;
+  const double* src = src_arr + base;
+  for (int e = tid; e < m * m; e += nt) ls_cp_async8(&tile[(e / m) * P + e % m], src + e);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  for (int i = tid; i < m; i += nt) {   // direction 2: row i
+    band_sweep_s<W, true>(tile + (size_t)i * P, 1, gF, gI, m, kc);
+    band_sweep_s<W, false>(tile + (size_t)i * P, 1, gB, gI, m, kc);
+  }
+  __syncthreads();
+  for (int j = tid; j < m; j += nt) {   // direction 1: column j
+    band_sweep_s<W, true>(tile + j, P, gF, gI, m, kc);
+    band_sweep_s<W, false>(tile + j, P, gB, gI, m, kc);
+  }
+  __syncthreads();
+  constexpr int U = 4;   // mode 1: the x_acc reads of U elements are issued before their stores
+  for (int e0 = tid; e0 < m * m; e0 += U * nt) {
+    double xa[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * nt;
+      xa[u] = (mode == 1 && e < m * m) ? xacc[base + e] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * nt;
+      if (e >= m * m) break;
+      const double v = tile[(e / m) * P + e % m];
+      if (mode == 0) data[base + e] = v;
+      else if (mode == 2) xacc[base + e] = omega * v;
+      else xacc[base + e] = fma(omega, v, xa[u]);
+    }
+  }
+}
+
+static size_t slab_smem(int m, int w) { return sizeof(double) * (size_t)(m + 2 * w) * (m | 1); }
+
+template <int W>
+static void launch_slab_w(double* data, int slabs, int m, const BandFactor& F, int mode, double omega, double* xacc,
+                          const double* src, cudaStream_t s) {
+  const size_t smem = slab_smem(m, W);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    IGACD_CUDA(cudaFuncSetAttribute(k_band_solve_slab<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const int nt = std::min(256, (m + 31) / 32 * 32);
+  k_band_solve_slab<W><<<slabs, nt, smem, s>>>(data, m, F.fac, F.kc, mode, omega, xacc, src);
+}
+
 // data <- F^{-1} data along axis `axis` of a [nc][m]^dim array; mode 1: xacc += omega * F^{-1} data
 // (data is then left holding the forward-substitution intermediate).
 void launch_band_solve(Handle& h, int nc, int level, int axis, const BandFactor& F, double* data, int mode,
@@ -495,6 +573,35 @@ void launch_band_solve(Handle& h, int nc, int level, int axis, const BandFactor&
     case 4: launch_w<4>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
     case 5: launch_w<5>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
     case 6: launch_w<6>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
+    default: throw Error{IGACD_E_ARG, "band width out of range"};
+  }
+  IGACD_LAUNCH_CHECK();
+  count_launch(h);
+}
+
+}  // namespace igacd
+
+namespace igacd {
+
+// two CTAs per SM at least: a lone 200+ KB CTA serialises load, sweeps and store (config 4,
+// m = 162: 23 % faster alone, slower inside the concurrent preconditioner)
+bool band_slab_fits(int m, int w) { return slab_smem(m, w) <= 113 * 1024 && m >= 2; }
+
+// 3D: data <- (F (x) F)^{-1} src over directions 1 and 2 of every slab of a [nc][m]^3 array
+// (modes as launch_band_solve)
+void launch_band_solve_slab(Handle& h, int nc, int level, const BandFactor& F, double* data, int mode, double omega,
+                            double* xacc, cudaStream_t s, const double* src) {
+  const int m = h.lv[level].m;
+  if (!src) src = data;
+  const int slabs = nc * m;
+  switch (F.w) {
+    case 0: launch_slab_w<0>(data, slabs, m, F, mode, omega, xacc, src, s); break;
+    case 1: launch_slab_w<1>(data, slabs, m, F, mode, omega, xacc, src, s); break;
+    case 2: launch_slab_w<2>(data, slabs, m, F, mode, omega, xacc, src, s); break;
+    case 3: launch_slab_w<3>(data, slabs, m, F, mode, omega, xacc, src, s); break;
+    case 4: launch_slab_w<4>(data, slabs, m, F, mode, omega, xacc, src, s); break;
+    case 5: launch_slab_w<5>(data, slabs, m, F, mode, omega, xacc, src, s); break;
+    case 6: launch_slab_w<6>(data, slabs, m, F, mode, omega, xacc, src, s); break;
     default: throw Error{IGACD_E_ARG, "band width out of range"};
   }
   IGACD_LAUNCH_CHECK();
