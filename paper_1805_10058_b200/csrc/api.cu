@@ -130,6 +130,8 @@ static void destroy_handle(Handle* h) {
   if (h->ga1) cudaEventDestroy(h->ga1);
   if (h->cap) cudaStreamDestroy(h->cap);
   if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
+  if (h->vec_stream) cudaStreamDestroy(h->vec_stream);
+  if (h->ev_join2) cudaEventDestroy(h->ev_join2);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (auto& pr : h->ev_pending) {
@@ -452,6 +454,15 @@ static void aux_solve(Handle& h, const double* sb, double* sx, cudaStream_t s) {
 // symmetric multiplicative combination of the auxiliary-space correction on span{b0 s}
 // (B_s = scalar V-cycle of A_s = Pi^T A Pi) and the vector V-cycle:
 //   z = Pi B_s Pi^T r;  z += V (r - A z);  z += Pi B_s Pi^T (r - A z).
+static bool prio_enabled() {   // IGACD_PRIO=0: the vector branch at default priority
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IGACD_PRIO");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static void precond_apply(Handle& h, const double* r, double* z, cudaStream_t s) {
   if (h.precond == PRECOND_VCYCLE || !h.has_aux) {
     vcycle_level(h, 0, 0, r, z, s);
@@ -464,18 +475,28 @@ static void precond_apply(Handle& h, const double* r, double* z, cudaStream_t s)
   if (h.precond == PRECOND_AUX_ADD) {   // additive (R8'): z = V r + Pi B_s Pi^T r
     // the two corrections are independent: the scalar branch runs on a second stream
     // (fork/join events; captured as parallel graph branches)
+    // The vector V-cycle is the critical path: it runs on a high-priority stream so its
+    // kernels take SMs first and the scalar branch fills the gaps (node priorities are kept
+    // in the captured graphs, cudaGraphInstantiateFlagUseNodePriority).
     if (!h.aux_stream) {
-      IGACD_CUDA(cudaStreamCreateWithFlags(&h.aux_stream, cudaStreamNonBlocking));
+      int lo = 0, hi = 0;
+      IGACD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      IGACD_CUDA(cudaStreamCreateWithPriority(&h.aux_stream, cudaStreamNonBlocking, lo));
+      IGACD_CUDA(cudaStreamCreateWithPriority(&h.vec_stream, cudaStreamNonBlocking, prio_enabled() ? hi : lo));
       IGACD_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
       IGACD_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
+      IGACD_CUDA(cudaEventCreateWithFlags(&h.ev_join2, cudaEventDisableTiming));
     }
     IGACD_CUDA(cudaEventRecord(h.ev_fork, s));
     IGACD_CUDA(cudaStreamWaitEvent(h.aux_stream, h.ev_fork, 0));
+    IGACD_CUDA(cudaStreamWaitEvent(h.vec_stream, h.ev_fork, 0));
     launch_pi_t(h, r, a0.b, h.aux_stream);
     aux_solve(h, a0.b, a0.x, h.aux_stream);
     IGACD_CUDA(cudaEventRecord(h.ev_join, h.aux_stream));
-    vcycle_level(h, 0, 0, r, z, s);
+    vcycle_level(h, 0, 0, r, z, h.vec_stream);
+    IGACD_CUDA(cudaEventRecord(h.ev_join2, h.vec_stream));
     IGACD_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
+    IGACD_CUDA(cudaStreamWaitEvent(s, h.ev_join2, 0));
     launch_pi(h, a0.x, z, true, s);
     return;
   }
@@ -530,7 +551,7 @@ static cudaGraphExec_t capture(Handle& h, F&& body, long long* nk) {
   }
   IGACD_CUDA(cudaStreamEndCapture(h.cap, &g));
   cudaGraphExec_t ex = nullptr;
-  const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+  const cudaError_t e = cudaGraphInstantiate(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
   cudaGraphDestroy(g);
   IGACD_CUDA(e);
   *nk = h.launches - before;

@@ -146,7 +146,8 @@ struct Handle {
   // CUDA graphs of the PCG iteration (api.cu): A = apply + x/r update + ||r||^2 -> host,
   // B = preconditioner + (r, z) + p update; captured on `cap`, replayed on the caller's stream
   cudaStream_t aux_stream = nullptr;          // concurrent branch of the additive preconditioner
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t vec_stream = nullptr;          // its critical branch (vector V-cycle), high priority
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   bool graphs = true;               // igacd_set_graphs (and IGACD_GRAPH=0 in the environment)
   cudaStream_t cap = nullptr;
   cudaGraphExec_t gA = nullptr, gB = nullptr;
