@@ -27,7 +27,7 @@ for ci in [int(a) for a in sys.argv[1:]] or [2, 3, 4]:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    print(json.dumps({"config": c.name, "minb": os.environ.get("IGACD_MINB", "2"), "ndof": N, "apply_ms": round(ms, 4),
+    print(json.dumps({"config": c.name, "ndof": N, "apply_ms": round(ms, 4),
                       "gdof_s": round(N / ms / 1e6, 2), "alg_GBs": round(16 * N / ms / 1e6, 1),
                       "hbm_frac": round(16 * N / ms / 1e6 / 6538.6, 4)}), flush=True)
     ig.igacd_destroy(h)
