@@ -484,3 +484,30 @@ def test_tsolve_matches_oracle(case):
             assert_close(to_host(x), H.Tlu[l].solve(b), 1e-12, "T^-1 level %d" % l)
     finally:
         ig.igacd_destroy(h)
+
+
+@pytest.mark.parametrize("case", [Case(2, 3, 64, nu=1e-2, beta=1e-3, b0=(S2, S2)),
+                                  Case(3, 2, 8, nu=0.3, beta=0.05, levels=2)], ids=repr)
+def test_aux_smoother_and_sweeps_match_oracle(case):
+    """Per-system options of the auxiliary V-cycle (igacd_set_aux_smoother / _sweeps) vs the oracle."""
+    h = case.handle()
+    try:
+        ig.igacd_set_aux_smoother(h, ig.IGACD_SMOOTH_JACOBI)
+        ig.igacd_set_aux_sweeps(h, 2, 2)
+        disc = Discretization(case.d, case.p, case.n)
+        A = disc.assemble(case.form)
+        B = AuxPreconditioner(A, case.d, case.p, case.n, case.b0, case.levels, mode="add", aux_smoother="jacobi",
+                              aux_nu_pre=2, aux_nu_post=2)
+        assert not B.exact
+        b = np.random.default_rng(17).uniform(-1, 1, disc.ndof)
+        x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")
+        ig.igacd_precond(h, to_dev(b), x)
+        tol = max(1e-12, 10 * np.finfo(float).eps * np.linalg.cond(B.V.A[-1].toarray()))
+        assert_close(to_host(x), B(b), tol, "aux jacobi x2 precond")
+        xo, ito, _ = pcg(A, b, B, 1e-8, 3000)
+        x.zero_()
+        it, rel = ig.igacd_solve(h, to_dev(b), x, 1e-8, 3000)
+        assert abs(it - ito) <= 1 and rel < 1e-8
+        assert np.linalg.norm(to_host(x) - xo) / np.linalg.norm(xo) <= 1e-8
+    finally:
+        ig.igacd_destroy(h)
