@@ -96,6 +96,18 @@ __global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ i
   double* xin = sm2;                       // [IR][ICP]
   double* tmp = sm2 + IR * ICP;            // [IR][TO2]
   const double* src = in + (size_t)blockIdx.z * nin * nin;
+  double* dst = out + (size_t)blockIdx.z * nout * nout;
+  // accumulate: the outputs' old values are requested first, so their DRAM latency hides
+  // behind the window load and both contractions (each thread owns OPT outputs)
+  constexpr int OPT = TO1 * TO2 / NT2;
+  static_assert(TO1 * TO2 % NT2 == 0, "whole outputs per thread");
+  double old[OPT];
+#pragma unroll
+  for (int u = 0; u < OPT; ++u) {
+    const int e = threadIdx.x + u * NT2;
+    const int o1 = o1a + e / TO2, c2 = e % TO2;
+    old[u] = (accumulate && o1 < o1b && o2a + c2 < o2b) ? dst[(size_t)o1 * nout + o2a + c2] : 0.0;
+  }
   for (int e = threadIdx.x; e < IR * IC; e += NT2) {
     const int r = e / IC, c = e - r * IC;
     xin[r * ICP + c] = __ldg(src + (size_t)(i1a + r) * nin + i2a + c);
@@ -118,8 +130,9 @@ __global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ i
   }
   __syncthreads();
   // axis 1: out[o1][o2] = sum_k T[o1][k] tmp[st(o1) - i1a + k][c2]
-  double* dst = out + (size_t)blockIdx.z * nout * nout;
-  for (int e = threadIdx.x; e < TO1 * TO2; e += NT2) {
+#pragma unroll
+  for (int u = 0; u < OPT; ++u) {
+    const int e = threadIdx.x + u * NT2;
     const int r1 = e / TO2, c2 = e - r1 * TO2;
     const int o1 = o1a + r1;
     if (o1 >= o1b || c2 >= nc2) continue;
@@ -129,9 +142,7 @@ __global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ i
     const double* tr = tmp + (st - i1a) * TO2 + c2;
     double acc = 0.0;
     for (int k = 0; k < kn; ++k) acc = fma(__ldg(wr + k), tr[k * TO2], acc);
-    double* d = dst + (size_t)o1 * nout + o2a + c2;
-    if (accumulate) *d += acc;
-    else *d = acc;
+    dst[(size_t)o1 * nout + o2a + c2] = old[u] + acc;   // old = 0 unless accumulating
   }
 }
 
