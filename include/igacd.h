@@ -118,6 +118,9 @@ int igacd_get_preconditioner(igacd_handle h, int* mode);
  * coordinate axis) and is inverted exactly by line solves instead of a V-cycle. */
 #define IGACD_SMOOTH_JACOBI 0
 #define IGACD_SMOOTH_TOEPLITZ 1
+/* T_n^p on the finest level only, damped Jacobi on the coarser ones (the paper's placement of
+ * the T_n^p smoother) */
+#define IGACD_SMOOTH_TOEPLITZ_FINE 2
 int igacd_set_smoother(igacd_handle h, int kind);
 /* Smoother of the auxiliary scalar V-cycle: IGACD_SMOOTH_JACOBI, IGACD_SMOOTH_TOEPLITZ, or -1
  * (default) for the same smoother as the vector V-cycle.  IGACD_E_ARG without an auxiliary space. */

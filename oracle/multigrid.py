@@ -126,7 +126,11 @@ class Hierarchy:
         return x
 
     def smooth(self, l, b, x, sweeps):
-        return (self.toeplitz if self.smoother == "toeplitz" else self.jacobi)(l, b, x, sweeps)
+        """smoother "toeplitz" (R4'), "jacobi" (R4), or "toeplitz_fine": T_n^p on the finest level
+        only, damped Jacobi on the coarser ones -- where the paper places its T_n^p smoother
+        (PAPER.md:1075, 1260)."""
+        use_t = self.smoother == "toeplitz" or (self.smoother == "toeplitz_fine" and l == 0)
+        return (self.toeplitz if use_t else self.jacobi)(l, b, x, sweeps)
 
     def vcycle(self, b, l: int = 0):
         """One V-cycle for A_l e = b from a zero initial guess (steps 1-3)."""

@@ -385,6 +385,14 @@ static int smoother_of(const Handle& h, int sy) {   // the auxiliary system may 
   return (sy == 1 && h.aux_smoother >= 0) ? h.aux_smoother : h.smoother;
 }
 
+// the smoother on level l: TOEPLITZ_FINE is the paper's placement of T_n^p -- the finest
+// level only -- with damped Jacobi on the coarser levels
+static int level_smoother(const Handle& h, int sy, int l) {
+  const int k = smoother_of(h, sy);
+  if (k == SMOOTH_TOEPLITZ_FINE) return l == 0 ? SMOOTH_TOEPLITZ : SMOOTH_JACOBI;
+  return k;
+}
+
 static void smooth(Handle& h, int sy, int l, const double* b, double*& cur, double*& oth, int sweeps, bool from_zero,
                    cudaStream_t s) {
   SysLevel& L = h.sys[sy].lv[l];
@@ -392,7 +400,7 @@ static void smooth(Handle& h, int sy, int l, const double* b, double*& cur, doub
     if (from_zero) launch_zero(h, cur, L.ndof, s);
     return;
   }
-  if (smoother_of(h, sy) == SMOOTH_JACOBI) {
+  if (level_smoother(h, sy, l) == SMOOTH_JACOBI) {
     int k = 0;
     if (from_zero) {
       launch_scale_dinv(h, sy, l, b, cur, L.omega, s);   // first sweep from x = 0: x = omega D^-1 b
@@ -425,7 +433,7 @@ static void vcycle_level(Handle& h, int sy, int l, const double* b, double* x, c
     return;
   }
   SysLevel& L = S.lv[l];
-  const int swaps = smoother_of(h, sy) == SMOOTH_JACOBI ? std::max(0, S.nu_pre - 1) + S.nu_post : 0;
+  const int swaps = level_smoother(h, sy, l) == SMOOTH_JACOBI ? std::max(0, S.nu_pre - 1) + S.nu_post : 0;
   double* cur = (swaps % 2 == 0) ? x : L.t;
   double* oth = (cur == x) ? L.t : x;
   smooth(h, sy, l, b, cur, oth, S.nu_pre, true, s);
@@ -866,7 +874,7 @@ int igacd_smoother_omega(igacd_handle h, int level, double* omega, double* rho) 
   check_level(H(h), level);
   Handle* hh = H(h);
   const SysLevel& L = hh->sys[0].lv[level];
-  const bool t = hh->smoother == SMOOTH_TOEPLITZ;
+  const bool t = level_smoother(*hh, 0, level) == SMOOTH_TOEPLITZ;
   if (omega) *omega = t ? L.omega_t : L.omega;
   if (rho) *rho = t ? L.rho_t : L.rho;
   API_END
@@ -979,7 +987,8 @@ int igacd_set_preconditioner(igacd_handle h, int mode) {
 
 int igacd_set_smoother(igacd_handle h, int kind) {
   API_BEGIN
-  if (kind != SMOOTH_JACOBI && kind != SMOOTH_TOEPLITZ) throw Error{IGACD_E_ARG, "unknown smoother"};
+  if (kind != SMOOTH_JACOBI && kind != SMOOTH_TOEPLITZ && kind != SMOOTH_TOEPLITZ_FINE)
+    throw Error{IGACD_E_ARG, "unknown smoother"};
   if (H(h)->smoother != kind) graphs_reset(*H(h));
   H(h)->smoother = kind;
   API_END
@@ -1008,7 +1017,8 @@ int igacd_set_aux_smoother(igacd_handle h, int kind) {
   API_BEGIN
   Handle* hh = H(h);
   if (!hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space on this handle"};
-  if (kind != -1 && kind != SMOOTH_JACOBI && kind != SMOOTH_TOEPLITZ) throw Error{IGACD_E_ARG, "unknown smoother"};
+  if (kind != -1 && kind != SMOOTH_JACOBI && kind != SMOOTH_TOEPLITZ && kind != SMOOTH_TOEPLITZ_FINE)
+    throw Error{IGACD_E_ARG, "unknown smoother"};
   if (hh->aux_smoother != kind) graphs_reset(*hh);
   hh->aux_smoother = kind;
   API_END
@@ -1054,7 +1064,7 @@ int igacd_aux_omega(igacd_handle h, int level, double* omega, double* rho) {
   check_level(hh, level);
   if (!hh->has_aux) throw Error{IGACD_E_ARG, "no auxiliary space on this handle"};
   const SysLevel& L = hh->sys[1].lv[level];
-  const bool t = smoother_of(*hh, 1) == SMOOTH_TOEPLITZ;
+  const bool t = level_smoother(*hh, 1, level) == SMOOTH_TOEPLITZ;
   if (omega) *omega = t ? L.omega_t : L.omega;
   if (rho) *rho = t ? L.rho_t : L.rho;
   API_END

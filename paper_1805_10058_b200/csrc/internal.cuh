@@ -82,7 +82,7 @@ struct Level {
   BandFactor T;  // Cholesky factor of T_{m}(m_{p-1}), the smoother's 1D factor
 };
 
-enum Smoother { SMOOTH_JACOBI = 0, SMOOTH_TOEPLITZ = 1 };
+enum Smoother { SMOOTH_JACOBI = 0, SMOOTH_TOEPLITZ = 1, SMOOTH_TOEPLITZ_FINE = 2 };
 
 // Per-level state of one system.
 struct SysLevel {

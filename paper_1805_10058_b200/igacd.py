@@ -72,6 +72,7 @@ IGACD_PRECOND_AUX = 1
 IGACD_PRECOND_AUX_ADD = 2
 IGACD_SMOOTH_JACOBI = 0
 IGACD_SMOOTH_TOEPLITZ = 1
+IGACD_SMOOTH_TOEPLITZ_FINE = 2
 
 
 class IgacdError(RuntimeError):

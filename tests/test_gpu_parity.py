@@ -209,19 +209,23 @@ VCYCLE_CASES = [Case(2, 2, 16, nu=1.0, beta=1e-2, lam=1.0, b0=(1.0, 0.0), levels
                 Case(3, 2, 8, nu=1.0, beta=0.1, levels=2), Case(3, 3, 8, nu=1.0, levels=2)]
 
 
-@pytest.mark.parametrize("smoother", ["toeplitz", "jacobi"])
+SMOOTHERS = {"toeplitz": 1, "jacobi": 0, "toeplitz_fine": 2}   # IGACD_SMOOTH_*
+
+
+@pytest.mark.parametrize("smoother", ["toeplitz", "jacobi", "toeplitz_fine"])
 @pytest.mark.parametrize("case", VCYCLE_CASES, ids=repr)
 def test_vcycle_matches_oracle(case, smoother):
     h = case.handle()
     try:
-        ig.igacd_set_smoother(h, ig.IGACD_SMOOTH_TOEPLITZ if smoother == "toeplitz" else ig.IGACD_SMOOTH_JACOBI)
+        ig.igacd_set_smoother(h, SMOOTHERS[smoother])
         disc = Discretization(case.d, case.p, case.n)
         A = disc.assemble(case.form)
         H = Hierarchy(A, case.d, case.p, case.n, case.levels, smoother=smoother)
         assert ig.igacd_num_levels(h) == len(H.ns)
         for l in range(len(H.ns) - 1):
             w, rho = ig.igacd_smoother_omega(h, l)
-            ref = H.rho_t[l] if smoother == "toeplitz" else H.rho[l]
+            use_t = smoother == "toeplitz" or (smoother == "toeplitz_fine" and l == 0)
+            ref = H.rho_t[l] if use_t else H.rho[l]
             assert abs(rho - ref) <= 1e-10 * ref, (l, rho, ref)
         b = np.random.default_rng(11).uniform(-1, 1, disc.ndof)
         x = torch.zeros(disc.ndof, dtype=torch.float64, device="cuda")

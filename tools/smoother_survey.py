@@ -15,7 +15,7 @@ for ci in [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4]:
     h = ig.igacd_create(c.dim, c.p, c.n, c.nu, c.beta, c.lam, c.b0, levels=c.levels)
     b = torch.from_numpy(inputs.rhs(c)).cuda()
     x = torch.zeros_like(b)
-    for sm in (ig.IGACD_SMOOTH_TOEPLITZ, ig.IGACD_SMOOTH_JACOBI):
+    for sm in (ig.IGACD_SMOOTH_TOEPLITZ, ig.IGACD_SMOOTH_TOEPLITZ_FINE, ig.IGACD_SMOOTH_JACOBI):
         ig.igacd_set_smoother(h, sm)
         for rep in range(2):
             torch.cuda.synchronize()
