@@ -460,6 +460,12 @@ static void launch_w(double* data, long long outer, int m, long long inner, cons
                      double omega, double* xacc, const double* src, cudaStream_t s) {
   // double-buffered 32-line tiles (2 warps) when they fit, else the widest single-buffered tile
   if (band_nbuf() == 2 && try_tiled<W, 2, 32, 2>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
+  // few long lines (2D: 2m per axis): 8-line tiles, so that more SMs run a recurrence
+  // (each tile's sweep is a serial chain of 2m steps whatever its width)
+  if (outer * inner < 8LL * num_sms() && try_tiled<W, 1, 4, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s))
+    return;
+  if (outer * inner < 64LL * num_sms() && try_tiled<W, 1, 8, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s))
+    return;
   // one warp per CTA packs 5 tiles per SM for m = 162 (2 warps per CTA: 4)
   if (band_warps() == 1 && try_tiled<W, 1, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
   if (try_tiled<W, 2, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
