@@ -150,16 +150,24 @@ class Discretization:
         for coef, F in terms:
             if coef == 0.0:
                 continue
-            Fr = F.reshape(E, Q, d * L, F.shape[-1])
-            K += coef * np.einsum("eq,eqac,eqbc->eab", W, Fr, Fr, optimize=True)
+            # K[e,a,b] += coef * sum_{q,c} W[e,q] F[e,q,a,c] F[e,q,b,c]: one matrix product per
+            # element (library primitive numpy.matmul) over the flattened (q, c) index
+            C = F.shape[-1]
+            Fr = F.reshape(E, Q, d * L, C)
+            X = Fr.transpose(0, 2, 1, 3).reshape(E, d * L, Q * C)
+            Xw = (Fr * W[:, :, None, None]).transpose(0, 2, 1, 3).reshape(E, d * L, Q * C)
+            K += coef * np.matmul(Xw, X.transpose(0, 2, 1))
         # global vector dof index: component j, scalar index
         gv = (np.arange(d)[None, :, None] * self.nscal + gidx[:, None, :]).reshape(E, d * L)
         vv = np.broadcast_to(valid[:, None, :], (E, d, L)).reshape(E, d * L)
         return K, gv, vv
 
-    def assemble(self, form, chunk=4096) -> sp.csr_matrix:
+    def assemble(self, form, chunk=None) -> sp.csr_matrix:
         """The full sparse matrix (test sizes only)."""
         elems = np.array(list(itertools.product(range(self.n), repeat=self.d)))
+        if chunk is None:   # elements per batch: ~150 MB of feature arrays
+            L = (self.p + 1) ** self.d
+            chunk = max(1, int(1.5e8 // (8 * L * L * self.d * self.d)))
         rows, cols, vals = [], [], []
         A = sp.csr_matrix((self.ndof, self.ndof))
         for s in range(0, len(elems), chunk):
