@@ -39,6 +39,8 @@ extern "C" {
 #define IGACD_E_CUDA (-2)     /* a CUDA runtime call or kernel launch failed                */
 #define IGACD_E_NOTSPD (-3)   /* coarse Cholesky met a non-positive pivot                    */
 #define IGACD_E_NOCONV (-4)   /* igacd_solve reached maxit without the requested residual   */
+#define IGACD_E_BREAKDOWN (-5) /* Krylov breakdown: (p, A p) <= 0, a zero Givens denominator, or
+                                  a non-finite residual (operator or preconditioner not SPD / NaN) */
 
 typedef struct igacd_handle_s* igacd_handle;
 
@@ -47,9 +49,10 @@ typedef struct igacd_handle_s* igacd_handle;
  *   nu, beta, lambda  >= 0 (nu > 0, beta in (1e-4, 1e-1], lambda = V_A dt)
  *   b0     host array of `dim` doubles, used as given (the configs pass unit vectors)
  *   levels 0 = automatic coarsening rule (reading R6), else exactly `levels` levels
- *   nu_pre, nu_post  damped-Jacobi sweeps before / after the coarse correction (reading R4)
+ *   nu_pre, nu_post  smoothing sweeps before / after the coarse correction, of whichever
+ *          smoother is active (default T_n^p Richardson, reading R4'; damped Jacobi, R4)
  * Work: 1D assembly (R1) and knot-insertion (R3) kernels, coarse inverse (R5), smoother
- * parameters by power iteration (R4).  Synchronises `stream`.  Owns all its device memory. */
+ * parameters by power iteration (R4, R4').  Synchronises `stream`.  Owns all its device memory. */
 int igacd_create(igacd_handle* out, int dim, int p, int n, double nu, double beta, double lambda,
                  const double* b0, int levels, int nu_pre, int nu_post, void* stream);
 
@@ -81,12 +84,13 @@ int igacd_residual(igacd_handle h, int level, const double* b, const double* x, 
  * omega > 0 is given (then used as is). */
 int igacd_smooth(igacd_handle h, int level, const double* b, double* x, int sweeps, double omega, void* stream);
 
-/* x_coarse = P_level^T x_fine   (R3, restriction to level+1). */
 /* x = T_l^{-1} b on `level` for the vector system: the smoother's preconditioner
  * T_n^p = I_d (x) T(m_{p-1}) (x) .. (x) T(m_{p-1}) (reading R4'), applied as
  * banded Cholesky line solves along each direction.  b, x: device, d*m^d doubles, no aliasing. */
 int igacd_tsolve(igacd_handle h, int level, const double* b, double* x, void* stream);
 
+/* x_coarse = P_level^T x_fine   (R3, restriction to level+1; PAPER.md:1111 R = P^T).
+ * x_fine: igacd_ndof(h, level) doubles, x_coarse: igacd_ndof(h, level+1) doubles, device. */
 int igacd_restrict(igacd_handle h, int level, const double* x_fine, double* x_coarse, void* stream);
 
 /* x_fine = P_level x_coarse (accumulate == 0) or x_fine += P_level x_coarse (accumulate != 0). */
@@ -133,10 +137,12 @@ int igacd_aux_is_exact(igacd_handle h, int* exact);
 int igacd_apply_aux(igacd_handle h, int level, const double* s_in, double* s_out, void* stream);
 int igacd_aux_omega(igacd_handle h, int level, double* omega, double* rho);
 
-/* PCG with the V-cycle preconditioner, zero initial guess, stop when
+/* PCG with the preconditioner selected by igacd_set_preconditioner (default: the additive
+ * auxiliary-space + V-cycle combination IGACD_PRECOND_AUX_ADD), zero initial guess, stop when
  * ||r_k||_2 / ||r_0||_2 < tol or after maxit iterations (R7).
  * iters, relres: host outputs (may be NULL).  Synchronises `stream`.
- * Returns IGACD_E_NOCONV (x still written) when maxit is reached. */
+ * Returns IGACD_E_NOCONV (x still written) when maxit is reached, IGACD_E_BREAKDOWN when
+ * (p, A p) <= 0 or the residual is not finite (iters/relres then hold the failing iteration). */
 int igacd_solve(igacd_handle h, const double* b, double* x, double tol, int maxit, int* iters,
                 double* relres, void* stream);
 

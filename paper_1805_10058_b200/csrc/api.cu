@@ -585,7 +585,8 @@ static void pcg_part_a(Handle& h, double* x, cudaStream_t s) {
   launch_finalize(h, h.partial, np, h.scal + S_PQ, s);
   launch_pcg_update_xr(h, x, h.pr, h.pp, h.pq, N, h.scal + S_RZ0, h.scal + S_PQ, h.partial, s);
   launch_finalize(h, h.partial, vec_ctas(N), h.scal + S_RR, s);
-  IGACD_CUDA(cudaMemcpyAsync(h.hscal + S_RR, h.scal + S_RR, sizeof(double), cudaMemcpyDeviceToHost, s));
+  // (p, A p) and ||r||^2 (adjacent slots) to the host: the stopping test and the breakdown check
+  IGACD_CUDA(cudaMemcpyAsync(h.hscal + S_PQ, h.scal + S_PQ, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
 }
 
 static void pcg_part_b(Handle& h, cudaStream_t s) {
@@ -642,6 +643,14 @@ static int pcg(Handle& h, const double* b, double* x, double tol, int maxit, int
       h.apply_ms += ms;
     }
     rel = std::sqrt(h.hscal[S_RR]) / r0;
+    // breakdown: A or B not SPD (p^T A p <= 0), or a non-finite value from the preconditioner
+    if (!(h.hscal[S_PQ] > 0.0) || !std::isfinite(rel)) {
+      if (iters) *iters = it;
+      if (relres) *relres = rel;
+      throw Error{IGACD_E_BREAKDOWN, "PCG breakdown at iteration " + std::to_string(it) +
+                                         ": (p, A p) = " + std::to_string(h.hscal[S_PQ]) +
+                                         ", relative residual " + std::to_string(rel)};
+    }
     if (rel < tol || it == maxit) break;
     if (use_graph) {
       IGACD_CUDA(cudaGraphLaunch(h.gB, s));
@@ -732,6 +741,9 @@ static int fgmres(Handle& h, const double* b, double* x, double tol, int maxit, 
         Hm(i + 1, j) = -sn[i] * a + cs[i] * c;
       }
       const double den = std::hypot(Hm(j, j), Hm(j + 1, j));
+      if (!(den > 0.0) || !std::isfinite(den))
+        throw Error{IGACD_E_BREAKDOWN, "GMRES breakdown at iteration " + std::to_string(it) +
+                                           ": Givens denominator " + std::to_string(den)};
       cs[j] = Hm(j, j) / den;
       sn[j] = Hm(j + 1, j) / den;
       Hm(j, j) = den;

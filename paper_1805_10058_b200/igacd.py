@@ -67,6 +67,7 @@ _get_prof = _sig("igacd_get_profile", [_vp, _P(ctypes.c_longlong), _P(ctypes.c_l
 _reset_prof = _sig("igacd_reset_profile", [_vp])
 
 IGACD_E_NOCONV = -4
+IGACD_E_BREAKDOWN = -5
 IGACD_PRECOND_VCYCLE = 0
 IGACD_PRECOND_AUX = 1
 IGACD_PRECOND_AUX_ADD = 2
@@ -86,12 +87,43 @@ def _check(rc):
         raise IgacdError(rc, _lib.igacd_last_error().decode())
 
 
-def _dptr(t):
+def _dptr(t, n=None):
+    """Device pointer of a contiguous CUDA float64 tensor holding exactly ``n`` elements
+    (the C side reads / writes n doubles through it, so a short or mistyped buffer is refused
+    here instead of corrupting device memory)."""
     if t is None:
         return None
-    if not (t.is_cuda and t.dtype.__str__() == "torch.float64" and t.is_contiguous()):
+    if not (getattr(t, "is_cuda", False) and str(t.dtype) == "torch.float64" and t.is_contiguous()):
         raise TypeError("expected a contiguous CUDA float64 tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError("vector has %d elements, the level needs %d" % (t.numel(), n))
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(a, n):
+    """Host pointer of a C-contiguous float64 numpy array or CPU tensor of exactly n elements."""
+    if hasattr(a, "data_ptr"):
+        if a.is_cuda or str(a.dtype) != "torch.float64" or not a.is_contiguous():
+            raise TypeError("expected a contiguous CPU float64 tensor")
+        if a.numel() != n:
+            raise ValueError("host vector has %d elements, the system needs %d" % (a.numel(), n))
+        return ctypes.c_void_p(a.data_ptr())
+    import numpy as np
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]):
+        raise TypeError("expected a C-contiguous float64 numpy array")
+    if a.size != n:
+        raise ValueError("host vector has %d elements, the system needs %d" % (a.size, n))
+    if not a.flags["WRITEABLE"]:
+        raise ValueError("host vector must be writeable")
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _nvec(h, level=0):
+    return igacd_ndof(h, level)
+
+
+def _nscal(h, level=0):
+    return igacd_ndof(h, level) // igacd_get_info(h)[0]
 
 
 def _stream(stream):
@@ -113,12 +145,17 @@ def igacd_version():
 
 
 def igacd_create(dim, p, n, nu, beta, lam, b0, levels=0, nu_pre=1, nu_post=1, stream=None):
+    if len(b0) != dim:
+        raise ValueError("b0 needs %d entries, got %d" % (dim, len(b0)))
     h = _vp()
     _check(_create(ctypes.byref(h), dim, p, n, nu, beta, lam, _darr(b0), levels, nu_pre, nu_post, _stream(stream)))
     return h
 
 
 def igacd_create_form(dim, p, n, mass, K, levels=0, nu_pre=1, nu_post=1, stream=None):
+    mass, K = list(mass), list(K)
+    if len(mass) != dim * dim or len(K) != dim ** 4:
+        raise ValueError("mass needs dim^2 = %d and K dim^4 = %d entries" % (dim * dim, dim ** 4))
     h = _vp()
     _check(_create_form(ctypes.byref(h), dim, p, n, _darr(list(mass)), _darr(list(K)), levels, nu_pre, nu_post,
                         _stream(stream)))
@@ -160,31 +197,31 @@ def igacd_smoother_omega(h, level):
 
 
 def igacd_apply(h, level, x, y, stream=None):
-    _check(_apply(h, level, _dptr(x), _dptr(y), _stream(stream)))
+    _check(_apply(h, level, _dptr(x, _nvec(h, level)), _dptr(y, _nvec(h, level)), _stream(stream)))
 
 
 def igacd_residual(h, level, b, x, r, stream=None):
-    _check(_residual(h, level, _dptr(b), _dptr(x), _dptr(r), _stream(stream)))
+    _check(_residual(h, level, *[_dptr(v, _nvec(h, level)) for v in (b, x, r)], _stream(stream)))
 
 
 def igacd_smooth(h, level, b, x, sweeps, omega=0.0, stream=None):
-    _check(_smooth(h, level, _dptr(b), _dptr(x), sweeps, omega, _stream(stream)))
+    _check(_smooth(h, level, _dptr(b, _nvec(h, level)), _dptr(x, _nvec(h, level)), sweeps, omega, _stream(stream)))
 
 
 def igacd_restrict(h, level, x_fine, x_coarse, stream=None):
-    _check(_restrict(h, level, _dptr(x_fine), _dptr(x_coarse), _stream(stream)))
+    _check(_restrict(h, level, _dptr(x_fine, _nvec(h, level)), _dptr(x_coarse, _nvec(h, level + 1)), _stream(stream)))
 
 
 def igacd_prolong(h, level, x_coarse, x_fine, accumulate=False, stream=None):
-    _check(_prolong(h, level, _dptr(x_coarse), _dptr(x_fine), 1 if accumulate else 0, _stream(stream)))
+    _check(_prolong(h, level, _dptr(x_coarse, _nvec(h, level + 1)), _dptr(x_fine, _nvec(h, level)), 1 if accumulate else 0, _stream(stream)))
 
 
 def igacd_vcycle(h, b, x, stream=None):
-    _check(_vcycle(h, _dptr(b), _dptr(x), _stream(stream)))
+    _check(_vcycle(h, _dptr(b, _nvec(h)), _dptr(x, _nvec(h)), _stream(stream)))
 
 
 def igacd_precond(h, b, x, stream=None):
-    _check(_precond(h, _dptr(b), _dptr(x), _stream(stream)))
+    _check(_precond(h, _dptr(b, _nvec(h)), _dptr(x, _nvec(h)), _stream(stream)))
 
 
 def igacd_set_preconditioner(h, mode):
@@ -214,7 +251,7 @@ def igacd_aux_is_exact(h):
 
 
 def igacd_apply_aux(h, level, s_in, s_out, stream=None):
-    _check(_apply_aux(h, level, _dptr(s_in), _dptr(s_out), _stream(stream)))
+    _check(_apply_aux(h, level, _dptr(s_in, _nscal(h, level)), _dptr(s_out, _nscal(h, level)), _stream(stream)))
 
 
 def igacd_aux_omega(h, level):
@@ -225,14 +262,14 @@ def igacd_aux_omega(h, level):
 
 def igacd_solve(h, b, x, tol, maxit, stream=None, raise_on_noconv=True):
     it, rel = _c_int(), _c_double()
-    rc = _solve(h, _dptr(b), _dptr(x), tol, maxit, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
+    rc = _solve(h, _dptr(b, _nvec(h)), _dptr(x, _nvec(h)), tol, maxit, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
     if rc != IGACD_E_NOCONV or raise_on_noconv:
         _check(rc)
     return it.value, rel.value
 
 
 def igacd_tsolve(h, level, b, x, stream=None):
-    _check(_tsolve(h, level, _dptr(b), _dptr(x), _stream(stream)))
+    _check(_tsolve(h, level, _dptr(b, _nvec(h, level)), _dptr(x, _nvec(h, level)), _stream(stream)))
 
 
 def igacd_set_aux_smoother(h, kind):
@@ -249,20 +286,18 @@ def igacd_set_graphs(h, enable):
 
 def igacd_gmres(h, b, x, tol, maxit, restart=30, stream=None, raise_on_noconv=True):
     it, rel = _c_int(), _c_double()
-    rc = _gmres(h, _dptr(b), _dptr(x), tol, maxit, restart, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
+    rc = _gmres(h, _dptr(b, _nvec(h)), _dptr(x, _nvec(h)), tol, maxit, restart, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
     if rc != IGACD_E_NOCONV or raise_on_noconv:
         _check(rc)
     return it.value, rel.value
 
 
 def igacd_solve_host(h, b_host, x_host, tol, maxit, stream=None, raise_on_noconv=True):
-    """b_host / x_host: C-contiguous float64 numpy arrays or CPU tensors (pinned or not)."""
-    def hp(a):
-        if hasattr(a, "data_ptr"):
-            return ctypes.c_void_p(a.data_ptr())
-        return a.ctypes.data_as(ctypes.c_void_p)
+    """b_host / x_host: C-contiguous float64 numpy arrays or CPU tensors (pinned or not) of
+    exactly igacd_ndof(h) elements (checked: the C side copies that many doubles)."""
+    N = _nvec(h)
     it, rel = _c_int(), _c_double()
-    rc = _solve_host(h, hp(b_host), hp(x_host), tol, maxit, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
+    rc = _solve_host(h, _hptr(b_host, N), _hptr(x_host, N), tol, maxit, ctypes.byref(it), ctypes.byref(rel), _stream(stream))
     if rc != IGACD_E_NOCONV or raise_on_noconv:
         _check(rc)
     return it.value, rel.value
