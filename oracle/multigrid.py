@@ -71,6 +71,29 @@ def toeplitz_T(p: int, m: int) -> np.ndarray:
     return T
 
 
+def toeplitz_solve_axes(p: int, m: int, d: int, nc: int, b: np.ndarray) -> np.ndarray:
+    """x = (I_nc (x) T(m_{p-1})^{(x) d})^{-1} b by the Kronecker identity
+    (T (x) T (x) T)^{-1} = T^{-1} (x) T^{-1} (x) T^{-1} ("each (T)^{-1} can be
+    solved by means of an LU factorization which is optimal for banded matrices"): one banded
+    Cholesky solve (library primitives scipy.linalg.cholesky_banded / cho_solve_banded) along each
+    axis of the [nc][m]^d array, all lines at once.  Same result as the sparse LU of the assembled
+    Kronecker product (pinned in tests), usable at sizes where that factorisation is too large."""
+    T = toeplitz_T(p, m)
+    w = p - 1
+    ab = np.zeros((w + 1, m))            # upper banded storage: ab[w + i - j, j] = T[i, j]
+    for j in range(m):
+        for i in range(max(0, j - w), j + 1):
+            ab[w + i - j, j] = T[i, j]
+    cb = sla.cholesky_banded(ab)
+    x = np.asarray(b, dtype=float).reshape((nc,) + (m,) * d)
+    for axis in range(1, d + 1):
+        y = np.moveaxis(x, axis, 0)
+        shp = y.shape
+        y = sla.cho_solve_banded((cb, False), y.reshape(m, -1))
+        x = np.moveaxis(y.reshape(shp), 0, axis)
+    return np.ascontiguousarray(x).reshape(-1)
+
+
 def power_rho_t(A: sp.spmatrix, Tsolve, steps: int = POWER_STEPS) -> float:
     """rho_t = ||T^{-1} A v|| after ``steps`` normalised steps of v <- T^{-1} A v (reading R4')."""
     v = hash_vector(A.shape[0])

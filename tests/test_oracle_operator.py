@@ -125,3 +125,53 @@ def test_2d_spectrum_follows_symbol(beta):
     if beta == 0.01:   # "about half of the spectrum is almost zero"
         frac = np.mean(ev < 0.05 * ev.max())
         assert 0.45 < frac < 0.55
+
+
+def _lambda_term_by_expansion(d, p, n, b0):
+    """lambda = 1 term of L_A assembled from the expanded form curl(b0 x u) = b0 div u - (b0 . grad) u
+    (constant b0), i.e. without any cross product: for psi = N e_j the integrand
+    vector is w(psi) = b0 d_j N - (b0 . grad N) e_j (3 entries; in 2D the third is 0).
+    An element loop written here, independent of oracle/operator.py's curl(b0 x psi) features;
+    only the B-spline tables (pinned in test_oracle_bspline.py) are shared."""
+    disc = Discretization(d, p, n)
+    import itertools
+    import scipy.sparse as sps
+    elems = np.array(list(itertools.product(range(n), repeat=d)))
+    W, Nv, G, gidx, valid = disc._element_data(elems)
+    E, Q, L = Nv.shape
+    b = np.zeros(3)
+    b[:d] = b0
+    w = np.zeros((E, Q, d, L, 3))            # w[e, q, j, l, :] for psi = N_l e_j
+    bgrad = np.einsum("eqlc,c->eql", G, np.asarray(b0, dtype=float))
+    for j in range(d):
+        for c in range(3):
+            w[:, :, j, :, c] = b[c] * G[..., j]
+        w[:, :, j, :, j] -= bgrad
+    rows, cols, vals = [], [], []
+    for e in range(E):
+        F = w[e].reshape(Q, d * L, 3)
+        Ke = np.einsum("q,qac,qbc->ab", W[e], F, F)
+        gv = (np.arange(d)[:, None] * disc.nscal + gidx[e][None, :]).reshape(-1)
+        vv = np.broadcast_to(valid[e][None, :], (d, L)).reshape(-1)
+        a_idx = np.nonzero(vv)[0]
+        rr, cc = np.meshgrid(gv[a_idx], gv[a_idx], indexing="ij")
+        rows.append(rr.ravel()); cols.append(cc.ravel()); vals.append(Ke[np.ix_(a_idx, a_idx)].ravel())
+    return sps.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                          shape=(disc.ndof, disc.ndof)).toarray()
+
+
+@pytest.mark.parametrize("d,p,n,b0", [(2, 2, 5, (0.6, 0.8)), (2, 3, 4, (2 ** -0.5, 2 ** -0.5)),
+                                      (3, 2, 3, (0.48, 0.6, 0.64)), (3, 3, 3, (3 ** -0.5,) * 3),
+                                      (3, 4, 2, (1.0, -2.0, 0.5))])
+def test_alfven_lambda_term_non_axis_b0_equals_expanded_form(d, p, n, b0):
+    # the oracle's lambda term (curl(b0 x psi) by np.cross) with all cross terms b0_i b0_j of a
+    # non-axis b0, against lambda ||b0 div u - (b0 . grad) u||^2 assembled independently
+    got = Discretization(d, p, n).assemble(form_alfven(0.0, 0.0, 1.0, b0)).toarray()
+    ref = _lambda_term_by_expansion(d, p, n, b0)
+    assert np.max(np.abs(got - ref)) < 1e-13 * np.max(np.abs(ref))
+    # and the whole form: nu (u,v) + beta lambda (div, div) + lambda (...) is linear in lambda
+    lam = 0.37
+    full = Discretization(d, p, n).assemble(form_alfven(0.2, 0.05, lam, b0)).toarray()
+    base = Discretization(d, p, n).assemble(form_alfven(0.2, 0.05, 0.0, b0)).toarray()
+    div = Discretization(d, p, n).assemble(form_curldiv(0.0, 1.0)).toarray()
+    assert np.max(np.abs(full - base - lam * ref - 0.05 * lam * div)) < 1e-13 * np.max(np.abs(full))
