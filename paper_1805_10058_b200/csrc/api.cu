@@ -121,7 +121,7 @@ static void destroy_handle(Handle* h) {
   cudaFree(h->partial);
   cudaFree(h->scal);
   if (h->hscal) cudaFreeHost(h->hscal);
-  for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar, h->zbuf}) cudaFree(v);
+  for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar}) cudaFree(v);
   for (double* v : {h->gm_v, h->gm_z, h->gm_partial, h->gm_dev}) cudaFree(v);
   if (h->gm_host) cudaFreeHost(h->gm_host);
   if (h->gA) cudaGraphExecDestroy(h->gA);
@@ -347,7 +347,6 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
     IGACD_CUDA(cudaMallocHost(&h->hscal, sizeof(double) * NSLOT));
     const size_t n0 = (size_t)dim * h->lv[0].nscal;
     for (double** v : {&h->pr, &h->pz, &h->pp, &h->pq, &h->aw, &h->ar}) IGACD_CUDA(cudaMalloc(v, sizeof(double) * n0));
-    if (dim == 3) IGACD_CUDA(cudaMalloc(&h->zbuf, sizeof(double) * 3 * n0));   // 3 * dim * m^3
     setup_system(*h, 0, dim, coef, s);
     // auxiliary space span{b0 s} (reading R8) when the b0-term is present
     const Coef ac = aux_patterns(dim, coef, h->b0);

@@ -134,7 +134,6 @@ struct Handle {
   // PCG / preconditioner vectors (level-0 size)
   double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *px = nullptr, *pb = nullptr;
   double *aw = nullptr, *ar = nullptr;   // aux preconditioner work (level-0 vector size)
-  double* zbuf = nullptr;                // 3D split operator: 3*nc per-point combinations (level-0 size)
   // FGMRES workspace (allocated on first use): Arnoldi basis V [restart+1][N], Z [restart][N]
   int gm_restart = 0;
   double* gm_v = nullptr;
@@ -190,6 +189,12 @@ int launch_operator(Handle& h, int sy, int level, const double* x, double* out, 
 int operator_ctas(const Handle& h, int level);                  // max over both systems
 int operator_ctas_sys(const Handle& h, int level, int nc);
 
+// ---- apply3d.cu ---------------------------------------------------------------------------
+// y = epilogue(A x) in 3D (one fused kernel per apply); grid and direction-0 chunk of a level
+void launch_apply3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                    cudaStream_t s);
+dim3 apply3d_grid(int m, int nc, int* chunk);
+
 // ---- transfer.cu --------------------------------------------------------------------
 void launch_prolong(Handle& h, int nc, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s);
 void launch_restrict(Handle& h, int nc, int level, const double* xf, double* xc, cudaStream_t s);
@@ -238,7 +243,11 @@ bool band_slab_fits(int m, int w);
 void launch_band_solve_slab(Handle& h, int nc, int level, const BandFactor& F, double* data, int mode, double omega,
                             double* xacc, cudaStream_t s, const double* src = nullptr);
 
-// ---- common -------------------------------------------------------------------------
+// ---- common.cu (device properties and kernel attributes, per device and thread-safe) -----
+int num_sms();                                                  // SMs of the current device
+void ensure_smem_attr(const void* func, size_t bytes);          // max dynamic shared memory >= bytes
+int max_active_blocks(const void* func, int threads, size_t smem);   // occupancy (cached)
+
 inline void count_launch(Handle& h) { h.launches++; }
 
 }  // namespace igacd

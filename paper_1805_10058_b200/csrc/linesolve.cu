@@ -396,39 +396,17 @@ void BandFactor::release() {
   Lb = inv = fac = nullptr;
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    IGACD_CUDA(cudaGetDevice(&dev));
-    IGACD_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
 template <int W, int WARPS, int TW, int NBUF>
 static bool try_tiled(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode,
                       double omega, double* xacc, const double* src, cudaStream_t s) {
   const size_t smem_t = sizeof(double) * ((size_t)WARPS * NBUF * (m + 2 * W) * (TW + 1));
   if (smem_t > 200 * 1024) return false;
-  static size_t attr_t = 0;
-  if (smem_t > 48 * 1024 && attr_t < smem_t) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_band_solve_tiled<W, WARPS, TW, NBUF>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
-    attr_t = smem_t;
-  }
+  const void* kern = (const void*)k_band_solve_tiled<W, WARPS, TW, NBUF>;
+  ensure_smem_attr(kern, smem_t);
   const long long groups = (outer * inner + TW - 1) / TW;
   long long blocks = (groups + WARPS - 1) / WARPS;
   // persistent grid: the factor is staged once per resident block, not once per tile
-  static size_t occ_smem = 0;
-  static int occ = 1;
-  if (occ_smem != smem_t) {
-    IGACD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_band_solve_tiled<W, WARPS, TW, NBUF>,
-                                                             32 * WARPS, smem_t));
-    occ = std::max(occ, 1);
-    occ_smem = smem_t;
-  }
+  const int occ = max_active_blocks(kern, 32 * WARPS, smem_t);
   blocks = std::min<long long>(blocks, (long long)occ * num_sms());
   k_band_solve_tiled<W, WARPS, TW, NBUF><<<(unsigned)blocks, 32 * WARPS, smem_t, s>>>(data, outer, m, inner, F.fac,
                                                                                     F.kc, mode, omega, xacc, src);
@@ -473,11 +451,7 @@ static void launch_w(double* data, long long outer, int m, long long inner, cons
   if (try_tiled<W, 1, 16, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
   if (try_tiled<W, 1, 8, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
   const size_t smem = sizeof(double) * ((size_t)m * (W + 1) + m);
-  static int attr_set = 0;
-  if (smem > 48 * 1024 && attr_set < (int)smem) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_band_solve<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = (int)smem;
-  }
+  ensure_smem_attr((const void*)k_band_solve<W>, smem);
   const long long lines = outer * inner;
   const int bs = 128;
   long long blocks = (lines + bs - 1) / bs;
@@ -553,11 +527,7 @@ template <int W>
 static void launch_slab_w(double* data, int slabs, int m, const BandFactor& F, int mode, double omega, double* xacc,
                           const double* src, cudaStream_t s) {
   const size_t smem = slab_smem(m, W);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_band_solve_slab<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  ensure_smem_attr((const void*)k_band_solve_slab<W>, smem);
   const int nt = std::min(256, (m + 31) / 32 * 32);
   k_band_solve_slab<W><<<slabs, nt, smem, s>>>(data, m, F.fac, F.kc, mode, omega, xacc, src);
 }

@@ -150,11 +150,7 @@ __global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ i
 static void transfer2d(Handle& h, const double* in, double* out, long long slabs, int nin, int nout, const int* start,
                        const double* w, int W, int win1, int win2, bool acc, cudaStream_t s) {
   const size_t smem = sizeof(double) * ((size_t)win1 * (win2 | 1) + (size_t)win1 * TO2);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    IGACD_CUDA(cudaFuncSetAttribute(k_transfer2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  ensure_smem_attr((const void*)k_transfer2d, smem);
   const dim3 grid((nout + TO2 - 1) / TO2, (nout + TO1 - 1) / TO1, (unsigned)slabs);
   k_transfer2d<<<grid, NT2, smem, s>>>(in, out, nin, nout, start, w, W, acc ? 1 : 0);
   IGACD_LAUNCH_CHECK();

@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libigacd.so")
+LIB_PATH = os.environ.get("IGACD_LIB") or os.path.join(_HERE, "lib", "libigacd.so")   # IGACD_LIB: debug builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError("libigacd.so not built (%s); run __graft_entry__.build()" % LIB_PATH)
