@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--maxit", type=int, default=20000)
-    ap.add_argument("--apply-reps", type=int, default=20)
+    ap.add_argument("--apply-reps", type=int, default=0,
+                    help="standalone applies per level in the sweep (default: 1000 for config 2, as BASELINE "
+                         "configs[2] asks, else 20)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
@@ -175,6 +177,50 @@ def max_over_ranks(value, dist, device):
     return float(t.item())
 
 
+def precond_timing(ig, h, b, stream, reps=10):
+    """Warm CUDA-event times of one vector V-cycle and one preconditioner application."""
+    import torch
+    z = torch.empty_like(b)
+    out = {}
+    for name, fn in (("vcycle_ms", ig.igacd_vcycle), ("precond_ms", ig.igacd_precond)):
+        for _ in range(2):
+            fn(h, b, z)
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(reps):
+            fn(h, b, z)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        out[name] = t0.elapsed_time(t1) / reps
+    return out
+
+
+def vcycle_bytes(ig, h, cfg):
+    """Algorithmic HBM bytes of one vector V-cycle from x = 0 with the T_n^p smoother, one pre-
+    and one post-sweep: every kernel reads each input once and writes
+    each output once, 8 B per fp64 value.  Per level with N unknowns (coarse level N' = N / 2^d):
+      pre-sweep   x = w T^-1 b: one line-solve pass per axis, 16 N each (3D levels whose [m][m]
+                  slab fits in shared memory solve axes 1 and 2 in one pass)
+      residual    r = b - A x: 24 N;   restriction r -> b': 8 N + 8 N'
+      prolongation x += P x': 8 N' + 16 N
+      post-sweep  r = b - A x (24 N), T^-1 passes (16 N each, the last one x += w .: 24 N)
+    coarsest level: the dense inverse (8 N^2) plus 16 N."""
+    L = ig.igacd_num_levels(h)
+    tot = 0.0
+    for l in range(L):
+        N = ig.igacd_ndof(h, l)
+        if l == L - 1:
+            tot += 8.0 * N * N + 16.0 * N
+            break
+        Nc = ig.igacd_ndof(h, l + 1)
+        passes = ig.igacd_level_tsolve_passes(h, l)
+        pre = 16.0 * N * passes
+        post = 24.0 * N + 16.0 * N * (passes - 1) + 24.0 * N
+        tot += pre + 24.0 * N + 8.0 * N + 8.0 * Nc + 8.0 * Nc + 16.0 * N + post
+    return tot
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -197,7 +243,11 @@ def main():
             dist.barrier()
 
     stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
     h = ig.igacd_create(cfg.dim, cfg.p, cfg.n, cfg.nu, cfg.beta, cfg.lam, cfg.b0, levels=cfg.levels)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup   # assembly, hierarchy, power iterations, coarse inverse
     N = ig.igacd_ndof(h)
     b_host = rank_rhs(cfg, rank)
     b = torch.from_numpy(b_host).cuda()
@@ -218,7 +268,7 @@ def main():
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         e0.record(stream)
-        its = []
+        its, rels = [], []
         for k in range(args.steps):
             if args.profile_step and k == 0:
                 torch.cuda.profiler.start()
@@ -226,6 +276,7 @@ def main():
             if args.profile_step and k == 0:
                 torch.cuda.profiler.stop()
             its.append(it)
+            rels.append(rel)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -234,6 +285,13 @@ def main():
     ig.igacd_set_profiling(h, False)
     ms = max_over_ranks(ms, dist, "cuda")
     value = N * world / (ms / 1000.0)
+    converged = all(r < cfg.tol for r in rels)
+    # self-check of the timed solves: the TRUE relative residual ||b - A x|| / ||b|| of the last
+    # solution (the library's residual kernel; PAPER.md:1333 criterion), not the recursive one
+    rv = torch.empty_like(b)
+    ig.igacd_residual(h, 0, b, x, rv)
+    true_relres = float(torch.linalg.norm(rv)) / float(torch.linalg.norm(b))
+    del rv
 
     # roofline of the dominant kernel (level-0 operator apply inside the timed solves)
     apply_avg_ms = apply_ms / max(apply_launches, 1)
@@ -264,21 +322,33 @@ def main():
                  "time_to_solution_s": g0.elapsed_time(g1) / 1000.0}
         del xg
 
-    # ---- operator-apply sweep (rotating buffers > L2) -----------------------------------
-    nbuf = max(2, int(np.ceil(2 * L2_BYTES / (16 * N))) + 1)
-    xs = [torch.randn(N, dtype=torch.float64, device="cuda") for _ in range(nbuf)]
-    ys = [torch.empty(N, dtype=torch.float64, device="cuda") for _ in range(nbuf)]
-    for k in range(3):
-        ig.igacd_apply(h, 0, xs[k % nbuf], ys[k % nbuf])
-    torch.cuda.synchronize()
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a0.record(stream)
-    for k in range(args.apply_reps):
-        ig.igacd_apply(h, 0, xs[k % nbuf], ys[k % nbuf])
-    a1.record(stream)
-    torch.cuda.synchronize()
-    sweep_ms = a0.elapsed_time(a1) / args.apply_reps
-    del xs, ys
+    # ---- one V-cycle and one preconditioner application (CUDA events, warm) --------------
+    vc = precond_timing(ig, h, b, stream)
+    vc_bytes = vcycle_bytes(ig, h, cfg)
+    vc_achieved = vc_bytes / (vc["vcycle_ms"] * 1e-3) / 1e9
+
+    # ---- operator-apply sweep over every level (rotating buffers > L2) ---------------------
+    reps = args.apply_reps or (1000 if args.config == 2 else 20)
+    sweep = []
+    for lvl in range(ig.igacd_num_levels(h)):
+        Nl = ig.igacd_ndof(h, lvl)
+        nbuf = max(2, int(np.ceil(2 * L2_BYTES / (16 * Nl))) + 1)
+        xs = [torch.randn(Nl, dtype=torch.float64, device="cuda") for _ in range(nbuf)]
+        ys = [torch.empty(Nl, dtype=torch.float64, device="cuda") for _ in range(nbuf)]
+        for k in range(3):
+            ig.igacd_apply(h, lvl, xs[k % nbuf], ys[k % nbuf])
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for k in range(reps):
+            ig.igacd_apply(h, lvl, xs[k % nbuf], ys[k % nbuf])
+        a1.record(stream)
+        torch.cuda.synchronize()
+        lms = a0.elapsed_time(a1) / reps
+        sweep.append({"level": lvl, "ndof": Nl, "ms": lms, "dof_per_s": Nl / (lms * 1e-3),
+                      "gbs": 16 * Nl / (lms * 1e-3) / 1e9, "reps": reps})
+        del xs, ys
+    sweep_ms = sweep[0]["ms"]
 
     # ---- end to end through the C ABI with host buffers -----------------------------------
     e2e = None
@@ -312,9 +382,10 @@ def main():
             "config": {"workload": cfg.name, "dim": cfg.dim, "p": cfg.p, "n": cfg.n, "ndof": N,
                        "nu": cfg.nu, "beta": cfg.beta, "lambda": cfg.lam, "b0": list(cfg.b0),
                        "levels": ig.igacd_num_levels(h), "tol": cfg.tol,
-                       "l2": "solve vectors exceed L2 (3D) / apply sweep rotates %d buffer pairs > 2xL2" % nbuf,
+                       "l2": "solve vectors exceed L2 (3D) / apply sweep rotates buffer pairs > 2xL2 per level",
                        "parallelism": "replicas" if world > 1 else "single"},
             "time_to_solution_s": ms / 1000.0, "pcg_iterations": its[-1], "relres": rel,
+            "converged": converged, "true_relres": true_relres, "setup_s": setup_s,
             "preconditioner": "aux-additive (R8') + V-cycle (Toeplitz smoother R4')",
             "apply": {"dof_per_s": N / (sweep_ms * 1e-3), "ms": sweep_ms,
                       "gbs": 16 * N / (sweep_ms * 1e-3) / 1e9,
@@ -327,6 +398,12 @@ def main():
             "roofline_fp64": {"bound": "alu", "achieved": fp64_achieved / 1e12, "peak": fp64_peak / 1e12,
                               "unit": "T FP64 instr/s", "frac": fp64_achieved / fp64_peak,
                               "per_unknown": fp64_per_unknown, "peak_source": "measured (tools/microbench)"},
+            "apply_sweep": sweep,
+            "vcycle": {"ms": vc["vcycle_ms"], "precond_ms": vc["precond_ms"], "bound": "hbm",
+                       "achieved": vc_achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                       "frac": vc_achieved / pk["hbm_gbs"], "alg_bytes": vc_bytes,
+                       "what": "one vector V-cycle (igacd_vcycle) from x = 0; algorithmic bytes per DESIGN.md "
+                               "'V-cycle bytes' (each kernel reads its inputs and writes its outputs once)"},
             "gmres": gmres,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -70,6 +70,9 @@ int igacd_get_info(igacd_handle h, int* dim, int* p, int* levels);
 int igacd_num_levels(igacd_handle h, int* levels);
 int igacd_level_n(igacd_handle h, int level, int* n);
 int igacd_ndof(igacd_handle h, int level, size_t* ndof);
+/* Line-solve passes of one T_n^p solve on `level` (reading R4'): dim, or 2
+ * in 3D when directions 1 and 2 of every [m][m] slab are solved in one shared-memory pass. */
+int igacd_level_tsolve_passes(igacd_handle h, int level, int* passes);
 /* omega and rho of the active smoother on `level` (Jacobi: rho(D^-1 A); Toeplitz: rho(T^-1 A)). */
 int igacd_smoother_omega(igacd_handle h, int level, double* omega, double* rho);
 

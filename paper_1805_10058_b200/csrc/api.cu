@@ -121,7 +121,7 @@ static void destroy_handle(Handle* h) {
   cudaFree(h->partial);
   cudaFree(h->scal);
   if (h->hscal) cudaFreeHost(h->hscal);
-  for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar}) cudaFree(v);
+  for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar, h->zbuf}) cudaFree(v);
   for (double* v : {h->gm_v, h->gm_z, h->gm_partial, h->gm_dev}) cudaFree(v);
   if (h->gm_host) cudaFreeHost(h->gm_host);
   if (h->gA) cudaGraphExecDestroy(h->gA);
@@ -337,6 +337,8 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
     IGACD_CUDA(cudaMalloc(&h->scratch0, sizeof(double) * scratch));
     IGACD_CUDA(cudaMalloc(&h->scratch1, sizeof(double) * scratch));
     size_t np = 1;
+    if (dim == 3 && split3d_enabled())   // 3 * dim * m^3 (level 0); set before the partial sizing below
+      IGACD_CUDA(cudaMalloc(&h->zbuf, sizeof(double) * 3 * (size_t)dim * h->lv[0].nscal));
     for (size_t l = 0; l < ns.size(); ++l) {
       np = std::max(np, (size_t)operator_ctas(*h, (int)l));
       np = std::max(np, (size_t)vec_ctas((size_t)dim * h->lv[l].nscal));
@@ -869,6 +871,15 @@ int igacd_level_n(igacd_handle h, int level, int* n) {
   check_ptr(n);
   check_level(H(h), level);
   *n = H(h)->lv[level].n;
+  API_END
+}
+
+int igacd_level_tsolve_passes(igacd_handle h, int level, int* passes) {
+  API_BEGIN
+  check_ptr(passes);
+  check_level(H(h), level);
+  const Handle& hh = *H(h);
+  *passes = (hh.dim == 3 && band_slab_enabled() && band_slab_fits(hh.lv[level].m, hh.lv[level].T.w)) ? 2 : hh.dim;
   API_END
 }
 

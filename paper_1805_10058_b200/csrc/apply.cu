@@ -251,7 +251,10 @@ static Grid grid_for(const Handle& h, int level, int nc) {
   return g;
 }
 
+static bool use_split(const Handle& h, int nc) { return h.dim == 3 && nc == 3 && h.zbuf; }
+
 int operator_ctas_sys(const Handle& h, int level, int nc) {
+  if (use_split(h, nc)) return split3d_ctas(h.lv[level].m);
   Grid g = grid_for(h, level, nc);
   return g.grid.x * g.grid.y * g.grid.z;
 }
@@ -278,9 +281,12 @@ int launch_operator(Handle& h, int sy, int level, const double* x, double* out, 
   const System& S = h.sys[sy];
   const OpParams& op = S.lv[level].op;
   Grid g = grid_for(h, level, S.nc);
-  const int nct = g.grid.x * g.grid.y * g.grid.z;
+  const int nct = operator_ctas_sys(h, level, S.nc);
   if (dot != DOT_NONE && (size_t)nct > h.partial_len) throw Error{IGACD_E_ARG, "partial buffer too small"};
-  if (h.dim == 3) {
+  if (use_split(h, S.nc)) {
+    launch_split3d(h.p, op, epi, mode, dot, x, out, h.zbuf, s);
+    count_launch(h);   // slab + column kernels
+  } else if (h.dim == 3) {
     launch_apply3d(h.p, S.nc, op, epi, mode, dot, x, out, s);
   } else {
     switch (h.p) {

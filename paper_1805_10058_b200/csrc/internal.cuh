@@ -134,6 +134,7 @@ struct Handle {
   // PCG / preconditioner vectors (level-0 size)
   double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *px = nullptr, *pb = nullptr;
   double *aw = nullptr, *ar = nullptr;   // aux preconditioner work (level-0 vector size)
+  double* zbuf = nullptr;                // 3D split operator (split3d.cu): 3 nc per-point combinations
   // FGMRES workspace (allocated on first use): Arnoldi basis V [restart+1][N], Z [restart][N]
   int gm_restart = 0;
   double* gm_v = nullptr;
@@ -194,6 +195,12 @@ int operator_ctas_sys(const Handle& h, int level, int nc);
 void launch_apply3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
                     cudaStream_t s);
 dim3 apply3d_grid(int m, int nc, int* chunk);
+
+// ---- split3d.cu: the vector system's slab + column kernels (z through zbuf) ---------------
+bool split3d_enabled();
+int split3d_ctas(int m);
+void launch_split3d(int p, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                    double* Z, cudaStream_t s);
 
 // ---- transfer.cu --------------------------------------------------------------------
 void launch_prolong(Handle& h, int nc, int level, const double* xc, double* xf, bool accumulate, cudaStream_t s);

@@ -37,6 +37,7 @@ _destroy = _sig("igacd_destroy", [_vp])
 _get_info = _sig("igacd_get_info", [_vp, _P(_c_int), _P(_c_int), _P(_c_int)])
 _num_levels = _sig("igacd_num_levels", [_vp, _P(_c_int)])
 _level_n = _sig("igacd_level_n", [_vp, _c_int, _P(_c_int)])
+_level_tsolve_passes = _sig("igacd_level_tsolve_passes", [_vp, _c_int, _P(_c_int)])
 _ndof = _sig("igacd_ndof", [_vp, _c_int, _P(_size_t)])
 _omega = _sig("igacd_smoother_omega", [_vp, _c_int, _P(_c_double), _P(_c_double)])
 _apply = _sig("igacd_apply", [_vp, _c_int, _vp, _vp, _vp])
@@ -181,6 +182,12 @@ def igacd_num_levels(h):
 def igacd_level_n(h, level):
     v = _c_int()
     _check(_level_n(h, level, ctypes.byref(v)))
+    return v.value
+
+
+def igacd_level_tsolve_passes(h, level):
+    v = _c_int()
+    _check(_level_tsolve_passes(h, level, ctypes.byref(v)))
     return v.value
 
 
