@@ -337,8 +337,12 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
     IGACD_CUDA(cudaMalloc(&h->scratch0, sizeof(double) * scratch));
     IGACD_CUDA(cudaMalloc(&h->scratch1, sizeof(double) * scratch));
     size_t np = 1;
-    if (dim == 3 && split3d_enabled())   // 3 * dim * m^3 (level 0); set before the partial sizing below
-      IGACD_CUDA(cudaMalloc(&h->zbuf, sizeof(double) * 3 * (size_t)dim * h->lv[0].nscal));
+    if (dim == 3) {   // z workspace of the split operator (the levels that take it): 3 * dim * m^3 doubles
+      size_t zmax = 0;
+      for (const Level& L : h->lv)
+        if (L.m % 2 == 1 || !apply3d_marching_pays(L.m) || split3d_forced()) zmax = std::max(zmax, L.nscal);
+      if (zmax) IGACD_CUDA(cudaMalloc(&h->zbuf, sizeof(double) * 3 * (size_t)dim * zmax));
+    }
     for (size_t l = 0; l < ns.size(); ++l) {
       np = std::max(np, (size_t)operator_ctas(*h, (int)l));
       np = std::max(np, (size_t)vec_ctas((size_t)dim * h->lv[l].nscal));

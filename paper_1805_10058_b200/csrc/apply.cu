@@ -246,15 +246,27 @@ static Grid grid_for(const Handle& h, int level, int nc) {
     nch = (m + g.chunk - 1) / g.chunk;
     g.grid = dim3(tx, nch, 1);
   } else {
-    g.grid = apply3d_grid(m, nc, &g.chunk);
+    g.grid = dim3(1, 1, 1);   // 3D grids are planned by the kernels' own launchers
+    g.chunk = 0;
   }
   return g;
 }
 
-static bool use_split(const Handle& h, int nc) { return h.dim == 3 && nc == 3 && h.zbuf; }
+// 3D paths: the persistent marching kernel (apply3d.cu; TMA staging on even-m levels, cp.async
+// on odd-m ones) for the scalar system and for the large even-m levels of the vector system;
+// the vector system's odd-m levels and the levels too small for marching to pay take the split
+// slab + column kernels (split3d.cu)
+static bool use_split(const Handle& h, int nc, int m) {
+  return h.dim == 3 && nc == 3 && h.zbuf && (m % 2 == 1 || !apply3d_marching_pays(m) || split3d_forced());
+}
 
 int operator_ctas_sys(const Handle& h, int level, int nc) {
-  if (use_split(h, nc)) return split3d_ctas(h.lv[level].m);
+  const int m = h.lv[level].m;
+  if (h.dim == 3) {   // upper bound over the paths a launch may take
+    int n = apply3d_ctas(h.p, nc, m);
+    if (nc == 3) n = std::max(n, split3d_ctas(m));
+    return n;
+  }
   Grid g = grid_for(h, level, nc);
   return g.grid.x * g.grid.y * g.grid.z;
 }
@@ -281,13 +293,14 @@ int launch_operator(Handle& h, int sy, int level, const double* x, double* out, 
   const System& S = h.sys[sy];
   const OpParams& op = S.lv[level].op;
   Grid g = grid_for(h, level, S.nc);
-  const int nct = operator_ctas_sys(h, level, S.nc);
+  int nct = operator_ctas_sys(h, level, S.nc);
   if (dot != DOT_NONE && (size_t)nct > h.partial_len) throw Error{IGACD_E_ARG, "partial buffer too small"};
-  if (use_split(h, S.nc)) {
+  if (use_split(h, S.nc, op.m)) {
     launch_split3d(h.p, op, epi, mode, dot, x, out, h.zbuf, s);
+    nct = split3d_ctas(op.m);
     count_launch(h);   // slab + column kernels
   } else if (h.dim == 3) {
-    launch_apply3d(h.p, S.nc, op, epi, mode, dot, x, out, s);
+    nct = launch_apply3d(h.p, S.nc, op, epi, mode, dot, x, out, s);
   } else {
     switch (h.p) {
       case 1: dispatch2d<1>(S.nc, g, op, epi, mode, dot, x, out, s); break;

@@ -191,13 +191,16 @@ int operator_ctas(const Handle& h, int level);                  // max over both
 int operator_ctas_sys(const Handle& h, int level, int nc);
 
 // ---- apply3d.cu ---------------------------------------------------------------------------
-// y = epilogue(A x) in 3D (one fused kernel per apply); grid and direction-0 chunk of a level
-void launch_apply3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
-                    cudaStream_t s);
-dim3 apply3d_grid(int m, int nc, int* chunk);
+// y = epilogue(A x) in 3D (one persistent fused kernel per apply); returns the CTAs launched
+// (= partial sums written when a DotMode is requested); apply3d_ctas: upper bound for a level
+int launch_apply3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                   cudaStream_t s);
+int apply3d_ctas(int p, int nc, int m);
+bool apply3d_marching_pays(int m);
 
-// ---- split3d.cu: the vector system's slab + column kernels (z through zbuf) ---------------
-bool split3d_enabled();
+
+// ---- split3d.cu: the vector system's slab + column kernels (z through zbuf), odd-m levels ---
+bool split3d_forced();   // IGACD_SPLIT=1: on every level (comparison)
 int split3d_ctas(int m);
 void launch_split3d(int p, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
                     double* Z, cudaStream_t s);

@@ -1,11 +1,12 @@
-// R2 in 3D, vector system (nc = 3): the round-1 split form of the operator, kept as the
-// product path while it is the faster one:
+// R2 in 3D, vector system (nc = 3): the round-1 split form of the operator.  It serves the
+// levels with odd m (rows not 16-byte aligned, so no TMA: ws3d.cu does not apply), where it
+// measured faster than the cp.async marching kernel of apply3d.cu:
 //   k_slab3d  one CTA per (in-slab tile, slab): directions 1 and 2 from shared memory and the
 //             9 per-point combinations z_{i,F0} written to global memory (zbuf);
 //   k_col3d   one thread per (direction-1, direction-2) column: the direction-0 band scatter into
 //             a register ring of 2p+1 output slabs per component, then the epilogue.
 // Same Kronecker patterns and Toeplitz/boundary-zone handling as apply3d.cu (eq:matr_Amu3D,
-// PAPER.md:515-543; boundary rows PAPER.md:347-354).  IGACD_SPLIT=0 selects the fused kernel.
+// PAPER.md:515-543; boundary rows PAPER.md:347-354).  IGACD_SPLIT=1 forces it on every level.
 #include <algorithm>
 #include <cstdlib>
 
@@ -341,10 +342,10 @@ void launch_split_p(const OpParams& op, const Epi& ep, int mode, int dot, const 
 
 }  // namespace
 
-bool split3d_enabled() {
+bool split3d_forced() {
   static const int v = [] {
-    const char* e = getenv("IGACD_SPLIT");
-    return (e && e[0] == '0') ? 0 : 1;
+    const char* e = getenv("IGACD_SPLIT");   // IGACD_SPLIT=1: the round-1 split form on every level
+    return (e && e[0] == '1') ? 1 : 0;
   }();
   return v == 1;
 }
