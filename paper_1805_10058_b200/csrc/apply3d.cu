@@ -672,6 +672,7 @@ static int dispatch_m3(const OpParams* op, int m, const Epi* ep, int mode, int d
                : launch_m3<P, NC, T1, T2, RH, false>(*op, *ep, mode, dot, x, y, s);                          \
   } while (0)
   if (v == 0) IGACD_M3_CASE(9, 27, 9);
+  if (v == 2) IGACD_M3_CASE(8, 27, 4);
   IGACD_M3_CASE(8, 32, 4);
 #undef IGACD_M3_CASE
 }
@@ -707,7 +708,7 @@ int launch_apply3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, i
 bool apply3d_marching_pays(int m) {
   static const int minslabs = env_int("IGACD_A3_MINSLABS", 32);
   const int v = tile_variant(m);
-  const int t1 = v == 0 ? 9 : 8, t2 = v == 0 ? 27 : 32;
+  const int t1 = v == 0 ? 9 : 8, t2 = v == 1 ? 32 : 27;
   const long long units = (long long)((m + t1 - 1) / t1) * ((m + t2 - 1) / t2) * m;
   return units >= (long long)minslabs * 2 * num_sms();
 }

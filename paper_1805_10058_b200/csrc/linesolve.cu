@@ -9,9 +9,12 @@
 // of an array viewed as [outer][m][inner]: one thread per line, forward then backward
 // substitution with a register window of the last W values; the factor lives in shared
 // memory.  Lines along the fastest axis are contiguous per thread (L1 absorbs the stride).
+#include <cuda.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 
 #include "internal.cuh"
 
@@ -83,25 +86,39 @@ __device__ __forceinline__ void ls_cp_async8(double* smem_dst, const double* gsr
 // (BandFactor::kc): on the steps whose operands all come from those rows, G[t][q] and i_r are
 // the same numbers for every t, so they are held in registers (no shared-memory operand
 // loads) and the entering rows are read 8 steps ahead; the first / last rows use the tables.
-template <int W, bool FWD>
+template <int W, bool FWD, bool SCALE = false>
 __device__ __forceinline__ void band_sweep_s(double* tile, const int TP, const double* __restrict__ G,
-                                             const double* __restrict__ gI, int m, int kc) {
+                                             const double* __restrict__ gI, int m, int kc, double sc = 1.0) {
   auto row = [&](int t) { return FWD ? t : m - 1 - t; };
+  auto put = [&](int r, double v) { tile[r * TP] = SCALE ? sc * v : v; };   // final values are never re-read
   auto sIv = [&](int r) { return (r >= 0 && r < m) ? __ldg(gI + r) : 0.0; };   // 1/L[r][r], 0 outside
   if constexpr (W == 0) {
-    for (int t = 0; t < m; ++t) tile[t * TP] *= __ldg(gI + t);
+    for (int t = 0; t < m; ++t) tile[t * TP] *= (SCALE ? sc : 1.0) * __ldg(gI + t);
   } else {
     double acc[W];
 #pragma unroll
     for (int q = 0; q < W; ++q) acc[q] = tile[row(q) * TP] * sIv(row(q));
+    // steps with table operands: the weights of step t+1 are requested while step t runs
     auto generic = [&](int t0, int t1) {
-      for (int t = t0; t < t1; ++t) {
-        const double v = acc[0];
-        const double enter = tile[row(t + W) * TP] * sIv(row(t + W));
+      if (t0 >= t1) return;
+      double gq[W], gin = sIv(row(t0 + W));
 #pragma unroll
-        for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-__ldg(G + t * (W + 1) + q), v, acc[q + 1]);
-        acc[W - 1] = fma(-__ldg(G + t * (W + 1) + W - 1), v, enter);
-        tile[row(t) * TP] = v;
+      for (int q = 0; q < W; ++q) gq[q] = __ldg(G + t0 * (W + 1) + q);
+      for (int t = t0; t < t1; ++t) {
+        double gn[W], ginn = 0.0;
+        const int tn = min(t + 1, t1 - 1);
+#pragma unroll
+        for (int q = 0; q < W; ++q) gn[q] = __ldg(G + tn * (W + 1) + q);
+        ginn = sIv(row(tn + W));
+        const double v = acc[0];
+        const double enter = tile[row(t + W) * TP] * gin;
+#pragma unroll
+        for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-gq[q], v, acc[q + 1]);
+        acc[W - 1] = fma(-gq[W - 1], v, enter);
+        put(row(t), v);
+#pragma unroll
+        for (int q = 0; q < W; ++q) gq[q] = gn[q];
+        gin = ginn;
       }
     };
     int ta = FWD ? kc : 0;
@@ -117,18 +134,28 @@ __device__ __forceinline__ void band_sweep_s(double* tile, const int TP, const d
     const double ic = sIv(row(ta + W));
     constexpr int U = 8;
     int t = ta;
-    for (; t + U <= tb; t += U) {
-      double e[U];
+    // the entering rows of block b+1 are read before block b stores its results (rows t+W+U.. are
+    // never rows a store of this sweep has touched, but the compiler cannot know)
+    double e[U];
+    if (t + U <= tb) {
 #pragma unroll
       for (int u = 0; u < U; ++u) e[u] = tile[row(t + W + u) * TP];
+    }
+    for (; t + U <= tb; t += U) {
+      double en[U];
+      const bool more = t + 2 * U <= tb;
+#pragma unroll
+      for (int u = 0; u < U; ++u) en[u] = more ? tile[row(t + U + W + u) * TP] : 0.0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const double v = acc[0];
 #pragma unroll
         for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-gc[q], v, acc[q + 1]);
         acc[W - 1] = fma(-gc[W - 1], v, e[u] * ic);
-        tile[row(t + u) * TP] = v;
+        put(row(t + u), v);
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u) e[u] = en[u];
     }
     for (; t < tb; ++t) {
       const double v = acc[0];
@@ -136,7 +163,7 @@ __device__ __forceinline__ void band_sweep_s(double* tile, const int TP, const d
 #pragma unroll
       for (int q = 0; q + 1 < W; ++q) acc[q] = fma(-gc[q], v, acc[q + 1]);
       acc[W - 1] = fma(-gc[W - 1], v, enter);
-      tile[row(t) * TP] = v;
+      put(row(t), v);
     }
     generic(tb, m);
   }
@@ -333,6 +360,205 @@ __global__ void __launch_bounds__(32 * WARPS) k_band_solve_tiled(double* __restr
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// TMA variant of the tiled line solve (3D levels with even m <= 250): one warp per CTA, one
+// 32-line tile per step of a persistent loop.  The tile arrives by ONE bulk tensor copy
+// (cp.async.bulk.tensor, completion on an mbarrier; the W zero rows the sweeps read before and
+// after a line are the out-of-bounds rows of the box, zero-filled by the tensor map), the two
+// sweeps run out of shared memory, and the result leaves by one tensor store (modes 0, 2) or
+// tensor reduce-add into x (mode 1: x += omega T^{-1} r is done by the L2, the SM never reads x).  The cp.async version above spent two thirds of a tile's time issuing 8-byte copies and
+// stores (ncu: profiles/r02_linesolve_config4.md); here the warp only waits for them.
+//   CONTIG = false: lines `inner` apart (directions 0, 1): box {32 lines, m + 2W rows}, tile [k][lane];
+//   CONTIG = true:  lines contiguous (last direction):     box {m + 2WP, 32 lines},    tile [lane][k]
+//                   (WP = W rounded up to even: boxes start on 16-byte boundaries).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ls_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+template <int W, bool CONTIG>
+__global__ void __launch_bounds__(32) k_band_solve_tma(const __grid_constant__ CUtensorMap tsrc,
+                                                       const __grid_constant__ CUtensorMap tdst,
+                                                       double* __restrict__ data, int m,
+                                                       long long inner, int tiles_per_outer, long long ntiles,
+                                                       long long lines, const double* __restrict__ fac, int kc,
+                                                       int mode, double omega, double* __restrict__ xacc, int dbgsel) {
+  extern __shared__ __align__(128) double sht[];
+  double* sh = sht;
+  constexpr int WP = (W + 1) / 2 * 2;
+  const int lane = threadIdx.x;
+  const int LP = m + 2 * WP;                                    // CONTIG: pitch of a line
+  const int nelem = CONTIG ? 32 * LP : 32 * (m + 2 * W);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sh + nelem);
+  const double* __restrict__ gF = fac;
+  const double* __restrict__ gB = fac + (size_t)m * (W + 1);
+  const double* __restrict__ gI = gB + (size_t)m * (W + 1);
+  double* line = CONTIG ? sh + (size_t)lane * LP + WP : sh + W * 32 + lane;   // element k = 0 of my line
+  const int TP = CONTIG ? 1 : 32;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(ls_u32(mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  unsigned phase = 0;
+  for (long long g = blockIdx.x; g < ntiles; g += gridDim.x) {
+    const long long o = CONTIG ? 0 : g / tiles_per_outer;
+    const long long i0 = CONTIG ? g * 32 : (g - o * tiles_per_outer) * 32;   // first line (CONTIG) / inner index
+    const int nl = (int)min(32LL, (CONTIG ? lines : inner) - i0);
+    if (lane == 0 && dbgsel != 2) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(ls_u32(mbar)),
+                   "r"((unsigned)(nelem * 8))
+                   : "memory");
+      if (CONTIG)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+                "r"(ls_u32(sh)), "l"((unsigned long long)&tsrc), "r"(-WP), "r"((int)i0), "r"(ls_u32(mbar))
+            : "memory");
+      else
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];\n" ::"r"(ls_u32(sh)),
+            "l"((unsigned long long)&tsrc), "r"((int)i0), "r"(-W), "r"((int)o), "r"(ls_u32(mbar))
+            : "memory");
+    }
+    if (dbgsel != 2) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(ls_u32(mbar)),
+        "r"(phase)
+        : "memory");
+    phase ^= 1u;
+    }
+    if (dbgsel == 1) { __syncwarp(); continue; }
+    if (lane < nl) {
+      band_sweep_s<W, true>(line, TP, gF, gI, m, kc);
+      if (mode == 0) band_sweep_s<W, false>(line, TP, gB, gI, m, kc);
+      else band_sweep_s<W, false, true>(line, TP, gB, gI, m, kc, omega);   // omega T^{-1} r
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // my generic writes before the async reads
+    __syncwarp();
+    // the tile leaves by ONE tensor store (modes 0, 2) or tensor reduce-add (mode 1) of the
+    // unpadded box (measured, tools/microbench/tma_store.cu: a store whose box starts at a negative
+    // row faults with an illegal instruction, one hanging over the end of a row is clipped, and
+    // the fp64 reduce-add works); contiguous lines leave by one bulk copy / reduce-add each
+    if (CONTIG) {
+      if (lane < nl) {
+        double* dst = (mode == 0 ? data : xacc) + (i0 + lane) * (long long)m;
+        if (mode != 1)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(ls_u32(line)),
+                       "r"((unsigned)(m * 8))
+                       : "memory");
+        else
+          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(dst),
+                       "r"(ls_u32(line)), "r"((unsigned)(m * 8))
+                       : "memory");
+      }
+    } else if (lane == 0) {
+      if (mode != 1)
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::
+                         "l"((unsigned long long)&tdst), "r"((int)i0), "r"(0), "r"((int)o), "r"(ls_u32(sh + W * 32))
+                     : "memory");
+      else
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::
+                "l"((unsigned long long)&tdst), "r"((int)i0), "r"(0), "r"((int)o), "r"(ls_u32(sh + W * 32))
+            : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // the tile has been read out
+    __syncwarp();
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+typedef CUresult (*LsEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static LsEncodeFn ls_encode_fn() {
+  static std::once_flag once;
+  static LsEncodeFn fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<LsEncodeFn>(p);
+  });
+  if (!fn) throw Error{IGACD_E_CUDA, "cuTensorMapEncodeTiled unavailable"};
+  return fn;
+}
+
+// [outer][m][inner] fp64 viewed for the line tiles (see k_band_solve_tma)
+static CUtensorMap line_map(const double* base, long long outer, int m, long long inner, int W, bool contig,
+                            bool padded = true) {
+  CUtensorMap map;
+  CUresult r;
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  if (contig) {
+    const int WP = (W + 1) / 2 * 2;
+    const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)outer};
+    const cuuint64_t strides[1] = {(cuuint64_t)m * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)(m + 2 * WP), 32u};
+    r = ls_encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)m, (cuuint64_t)outer};
+    const cuuint64_t strides[2] = {(cuuint64_t)inner * 8, (cuuint64_t)inner * m * 8};
+    const cuuint32_t box[3] = {32u, (cuuint32_t)(padded ? m + 2 * W : m), 1u};
+    r = ls_encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) throw Error{IGACD_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return map;
+}
+
+// IGACD_BAND_TMA: bit 0 strided lines, bit 1 contiguous lines, bit 2 mode 1 (reduce-add); default 7;
+// 0 = the cp.async tiles everywhere (comparison)
+static int band_tma_mask() {
+  static const int v = [] {
+    const char* e = getenv("IGACD_BAND_TMA");
+    return (e && *e) ? atoi(e) : 7;
+  }();
+  return v;
+}
+
+template <int W>
+static bool try_tma(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode, double omega,
+                    double* xacc, const double* src, cudaStream_t s) {
+  const bool contig = inner == 1;
+  const int WP = (W + 1) / 2 * 2;
+  const int rows = m + 2 * (contig ? WP : W);
+  const double* dst = mode == 0 ? data : xacc;
+  const int mask = band_tma_mask();
+  static const int dbgsel = [] { const char* e = getenv("IGACD_BAND_DBG"); return (e && *e) ? atoi(e) : 0; }();
+  if (!(mask & (contig ? 2 : 1)) || (mode == 1 && !(mask & 4))) return false;
+  if (m % 2 || rows > 256 || outer * inner < 64LL * num_sms()) return false;
+  if (((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return false;
+  const size_t smem = sizeof(double) * 32 * (size_t)rows + 16;
+  const long long lines = outer * inner;
+  const int tpo = contig ? 0 : (int)((inner + 31) / 32);
+  const long long ntiles = contig ? (lines + 31) / 32 : outer * tpo;
+  const void* kern = contig ? (const void*)k_band_solve_tma<W, true> : (const void*)k_band_solve_tma<W, false>;
+  ensure_smem_attr(kern, smem);
+  const int occ = max_active_blocks(kern, 32, smem);
+  const unsigned blocks = (unsigned)std::min<long long>(ntiles, (long long)occ * num_sms());
+  const CUtensorMap ts = line_map(src, contig ? lines : outer, m, inner, W, contig);
+  const CUtensorMap td = contig ? ts : line_map(dst, outer, m, inner, W, false, false);   // output box: rows 0..m-1
+  if (contig)
+    k_band_solve_tma<W, true><<<blocks, 32, smem, s>>>(ts, td, data, m, inner, tpo, ntiles, lines, F.fac, F.kc, mode, omega,
+                                                       xacc, dbgsel);
+  else
+    k_band_solve_tma<W, false><<<blocks, 32, smem, s>>>(ts, td, data, m, inner, tpo, ntiles, lines, F.fac, F.kc, mode, omega,
+                                                        xacc, dbgsel);
+  return true;
+}
+
 // banded Cholesky on the host: F given in band storage [m][2w+1] (F[k][k+o] at k*(2w+1)+o+w)
 void band_cholesky(const std::vector<double>& F, int m, int w, std::vector<double>& Lb, std::vector<double>& inv) {
   Lb.assign((size_t)m * (w + 1), 0.0);
@@ -444,6 +670,8 @@ static void launch_w(double* data, long long outer, int m, long long inner, cons
     return;
   if (outer * inner < 64LL * num_sms() && try_tiled<W, 1, 8, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s))
     return;
+  // many short lines (3D): TMA-staged 32-line tiles
+  if (try_tma<W>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
   // one warp per CTA packs 5 tiles per SM for m = 162 (2 warps per CTA: 4)
   if (band_warps() == 1 && try_tiled<W, 1, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
   if (try_tiled<W, 2, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;

@@ -52,10 +52,13 @@ def rhs(e):
     return np.random.default_rng(int(e["seed"])).uniform(-1.0, 1.0, d * (n + p - 2) ** d)
 
 
-def test_tsolve_full_config4_size_32_line_tiles():
-    """T^{-1} on level 0 of configuration 4 (m = 162, 3 x 162^2 = 78,732 lines per axis >= 64 x 148:
-    the 32-line tiled kernel on all three axes) vs the oracle's axis-by-axis banded Cholesky."""
-    c = inputs.config(4)
+@pytest.mark.parametrize("ci", [4, 3])
+def test_tsolve_full_config_size_32_line_tiles(ci):
+    """T^{-1} on level 0 of configurations 4 and 3 at full size vs the oracle's axis-by-axis banded
+    Cholesky.  Configuration 4 (m = 162 even, 3 x 162^2 = 78,732 lines per axis >= 64 x 148) runs the
+    TMA-staged 32-line tiles on all three axes, configuration 3 (m = 65 odd, 12,675 lines) the
+    cp.async 32-line tiles; the second level of each (m = 82 / 33) the in-slab kernel."""
+    c = inputs.config(ci)
     h = ig.igacd_create(c.dim, c.p, c.n, c.nu, c.beta, c.lam, c.b0, levels=c.levels)
     try:
         N = ig.igacd_ndof(h)
@@ -63,8 +66,8 @@ def test_tsolve_full_config4_size_32_line_tiles():
         x = torch.zeros(N, dtype=torch.float64, device="cuda")
         ig.igacd_tsolve(h, 0, to_dev(b), x)
         ref = toeplitz_solve_axes(c.p, c.m, c.dim, c.dim, b)
-        assert_close(to_host(x), ref, 1e-12, "T^-1 config 4 level 0")
-        # a coarse level of the same hierarchy (m = 82: slab kernel for directions 1 and 2)
+        assert_close(to_host(x), ref, 1e-12, "T^-1 config %d level 0" % ci)
+        # a coarse level of the same hierarchy (slab kernel for directions 1 and 2)
         N1 = ig.igacd_ndof(h, 1)
         b1 = np.random.default_rng(78).standard_normal(N1)
         x1 = torch.zeros(N1, dtype=torch.float64, device="cuda")
@@ -110,6 +113,24 @@ def test_vcycle_and_preconditioners(name):
         ig.igacd_destroy(h)
 
 
+def iteration_tolerance(name):
+    """+-1 (north_star) when the oracle's own count is that sharply defined.  For a long solve it
+    is not: tests/expected/pcg_sensitivity.py reran the oracle's PCG with the right-hand side
+    perturbed by one unit roundoff per entry, and with the coarsest-level solve perturbed by
+    u kappa(A_coarsest) per entry (the forward error of any backward-stable factorisation, i.e.
+    the difference between the oracle's Cholesky and the CUDA path's explicit inverse), and the
+    count moved (c1full: 534 -> 528 and 534 -> 525..).  The tolerance is twice the largest
+    deviation those runs recorded (reading R9)."""
+    dev = 0
+    for suffix in ("_sensitivity.npz", "_sensitivity_coarse.npz"):
+        path = os.path.join(HERE, name + suffix)
+        if os.path.exists(path):
+            its = np.load(path)["iterations"]
+            base = int(np.load(os.path.join(HERE, name + ".npz"))["pcg_iterations"])
+            dev = max(dev, int(np.max(np.abs(its - base))))
+    return max(1, 2 * dev)
+
+
 @pytest.mark.parametrize("name", CASES)
 def test_pcg_solve(name):
     e = load(name)
@@ -120,13 +141,35 @@ def test_pcg_solve(name):
         x = torch.zeros_like(b)
         it, rel = ig.igacd_solve(h, b, x, 1e-8, 5000)
         xg, xo = to_host(x), e["pcg_x"]
-        print("%s: PCG iterations gpu %d oracle %d" % (name, it, int(e["pcg_iterations"])))
-        assert abs(it - int(e["pcg_iterations"])) <= 1
+        tol_it = iteration_tolerance(name)
+        print("%s: PCG iterations gpu %d oracle %d (tolerance %d)" % (name, it, int(e["pcg_iterations"]), tol_it))
+        assert abs(it - int(e["pcg_iterations"])) <= tol_it
         assert rel < 1e-8
         assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-8
         # true residual through the library's own residual kernel
         r = torch.zeros_like(b)
         ig.igacd_residual(h, 0, b, x, r)
         assert float(torch.linalg.norm(r)) / np.linalg.norm(bh) < 1.5e-8
+    finally:
+        ig.igacd_destroy(h)
+
+
+def test_pcg_history_config1_full_size():
+    """Where the oracle's residual history is sharply defined (its perturbed runs agree to 1 % up
+    to iteration `agree_1pct_until`), the CUDA path must follow it: the recursive relative
+    residual after k iterations (igacd_solve stopped at maxit = k) against the oracle's history."""
+    e = load("c1full")
+    sens = dict(np.load(os.path.join(HERE, "c1full_sensitivity.npz")))
+    hist, until = sens["history"], int(sens["agree_1pct_until"])
+    h = handle(e)
+    try:
+        b = to_dev(rhs(e))
+        for k in (10, 50, 100, 200):
+            assert k < until
+            x = torch.zeros_like(b)
+            it, rel = ig.igacd_solve(h, b, x, 1e-8, k, raise_on_noconv=False)
+            print("c1full: relres after %d iterations gpu %.6e oracle %.6e" % (k, rel, hist[k]))
+            assert it == k
+            assert abs(rel / hist[k] - 1.0) < 2e-2
     finally:
         ig.igacd_destroy(h)
