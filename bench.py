@@ -392,7 +392,7 @@ def main():
                       "hbm_frac": 16 * N / (sweep_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk_src,
-                         "kernel": ("k_slab3d + k_col3d<p=%d> (level-0 apply inside PCG)" % cfg.p if cfg.dim == 3
+                         "kernel": ("k_march3d<p=%d> (level-0 apply inside PCG)" % cfg.p if cfg.dim == 3
                                     else "k_op2d<p=%d> (level-0 apply inside PCG)" % cfg.p),
                          "launches": apply_launches, "avg_ms": apply_avg_ms},
             "roofline_fp64": {"bound": "alu", "achieved": fp64_achieved / 1e12, "peak": fp64_peak / 1e12,

@@ -586,10 +586,13 @@ static int env_int(const char* name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
-// tile variants: 0 = 9 x 27 (m = 162: 18 x 6 tiles, no padding), 1 = 8 x 32
-static int tile_variant(int m) {
+// tile variants: 0 = 9 x 27 (m = 162: 18 x 6 tiles, no padding), 1 = 8 x 32.  The vector system
+// takes the one with fewer padded thread slots; the scalar system measured faster on 8 x 32 rows
+// of full warps even with the padding (config 4: 0.144 vs 0.163 ms).
+static int tile_variant(int m, int nc) {
   static const int force = env_int("IGACD_A3_TILE", -1);
   if (force >= 0) return force;
+  if (nc == 1) return 1;
   auto padded = [&](int t1, int t2, int nt) {   // thread slots per slab
     return (double)((m + t1 - 1) / t1) * ((m + t2 - 1) / t2) * nt;
   };
@@ -664,7 +667,7 @@ static int dispatch_m3(const OpParams* op, int m, const Epi* ep, int mode, int d
                        cudaStream_t s) {
   // TMA needs 16-byte aligned global rows (m even) and base address
   const bool tma = tma_enabled() && m % 2 == 0 && (!x || ((uintptr_t)x & 15) == 0);
-  const int v = tile_variant(m);
+  const int v = tile_variant(m, NC);
 #define IGACD_M3_CASE(T1, T2, RH)                                                                            \
   do {                                                                                                       \
     if (!op) return std::max(plan_m3<P, NC, T1, T2, RH, true>(m).ctas, plan_m3<P, NC, T1, T2, RH, false>(m).ctas); \
@@ -672,7 +675,6 @@ static int dispatch_m3(const OpParams* op, int m, const Epi* ep, int mode, int d
                : launch_m3<P, NC, T1, T2, RH, false>(*op, *ep, mode, dot, x, y, s);                          \
   } while (0)
   if (v == 0) IGACD_M3_CASE(9, 27, 9);
-  if (v == 2) IGACD_M3_CASE(8, 27, 4);
   IGACD_M3_CASE(8, 32, 4);
 #undef IGACD_M3_CASE
 }
@@ -707,8 +709,8 @@ int launch_apply3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, i
 // (2 x SMs).  Smaller levels of the vector system take the split slab + column kernels.
 bool apply3d_marching_pays(int m) {
   static const int minslabs = env_int("IGACD_A3_MINSLABS", 32);
-  const int v = tile_variant(m);
-  const int t1 = v == 0 ? 9 : 8, t2 = v == 1 ? 32 : 27;
+  const int v = tile_variant(m, 3);
+  const int t1 = v == 0 ? 9 : 8, t2 = v == 0 ? 27 : 32;
   const long long units = (long long)((m + t1 - 1) / t1) * ((m + t2 - 1) / t2) * m;
   return units >= (long long)minslabs * 2 * num_sms();
 }

@@ -6,9 +6,15 @@
 // the exact inverse of the auxiliary scalar operator when b0 is a coordinate direction,
 // A_s = (c_m M + c_s S)_l (x) M (x) .. (reading R8).
 // A factor F = L L^T (banded Cholesky, half bandwidth W <= 6) is applied along axis `a`
-// of an array viewed as [outer][m][inner]: one thread per line, forward then backward
-// substitution with a register window of the last W values; the factor lives in shared
-// memory.  Lines along the fastest axis are contiguous per thread (L1 absorbs the stride).
+// of an array viewed as [outer][m][inner].  Product kernels: one warp stages a tile of lines
+// in shared memory (lanes = lines) and every lane runs the forward and backward substitution
+// of its line in column order (band_sweep_s: one dependent DFMA per step; the factor tables
+// stay in global memory, L1-resident, and only the first / last rows of a sweep read them):
+//   k_band_solve_tma    3D levels with even m: 32-line tiles by one bulk tensor load and one
+//                       tensor store / reduce-add each;
+//   k_band_solve_tiled  every other case (cp.async staging; 4/8/32-line tiles);
+//   k_band_solve_slab   3D: directions 1 and 2 of a slab in one pass when the slab fits twice;
+//   k_band_solve        the in-place one-thread-per-line fallback.
 #include <cuda.h>
 
 #include <algorithm>

@@ -1,8 +1,11 @@
 // R3: prolongation x_f = (I_d (x) P (x) .. (x) P) x_c and restriction x_c = P^T x_f
-// (eq:2by2prol PAPER.md:1178-1186; R_l := P_l^T), one 1D pass per
-// direction.  Each pass views the array as [outer][axis][inner] and writes one output
-// element per thread from the fixed-width row storage of P (or P^T): coalesced along
-// `inner`, and for the fastest axis consecutive threads read overlapping windows.
+// (eq:2by2prol PAPER.md:1178-1186; R_l := P_l^T).  The two in-slab axes are
+// applied in ONE shared-memory pass (k_transfer2d: a CTA stages the input window of a 16 x 32
+// output tile, contracts axis 2 into an intermediate, then axis 1); 2D transfers are that
+// single pass, 3D transfers add one pass along axis 0 (k_axis_pass_rows), which views the array
+// as [outer][axis][inner] and writes one output element per thread from the fixed-width row
+// storage of P (or P^T), coalesced along `inner`.  k_axis_pass_fast is the 1D pass along the
+// fastest axis (consecutive threads read overlapping windows), used by the stage entry points.
 #include <algorithm>
 
 #include "internal.cuh"
@@ -83,9 +86,11 @@ static void axis_pass(Handle& h, const double* in, double* out, long long outer,
 // from DRAM once (window halos come from L2) instead of once per 1D pass.
 constexpr int TO1 = TRANSFER_TO1, TO2 = TRANSFER_TO2, NT2 = 256;
 
+template <int W>   // row width of the 1D transfer (compile time: the contraction loops unroll and
+                   // their weight loads are all in flight at once)
 __global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ in, double* __restrict__ out, int nin,
                                                     int nout, const int* __restrict__ start,
-                                                    const double* __restrict__ w, int W, int accumulate) {
+                                                    const double* __restrict__ w, int accumulate) {
   extern __shared__ __align__(16) double sm2[];
   const int o1a = blockIdx.y * TO1, o2a = blockIdx.x * TO2;
   const int o1b = min(o1a + TO1, nout), o2b = min(o2a + TO2, nout);
@@ -108,25 +113,35 @@ __global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ i
     const int o1 = o1a + e / TO2, c2 = e % TO2;
     old[u] = (accumulate && o1 < o1b && o2a + c2 < o2b) ? dst[(size_t)o1 * nout + o2a + c2] : 0.0;
   }
-  for (int e = threadIdx.x; e < IR * IC; e += NT2) {
-    const int r = e / IC, c = e - r * IC;
-    xin[r * ICP + c] = __ldg(src + (size_t)(i1a + r) * nin + i2a + c);
+  // window load: one warp per row, lanes along the row (no division by the runtime window width)
+  for (int r = threadIdx.x >> 5; r < IR; r += NT2 / 32) {
+    const double* srow = src + (size_t)(i1a + r) * nin + i2a;
+    double* xrow = xin + r * ICP;
+    for (int c = threadIdx.x & 31; c < IC; c += 32) xrow[c] = __ldg(srow + c);
   }
   __syncthreads();
-  // axis 2: tmp[r][c2] = sum_k T[o2][k] xin[r][st(o2) - i2a + k]
+  // axis 2: tmp[r][c2] = sum_k T[o2][k] xin[r][st(o2) - i2a + k].  Lane = output column (its W
+  // weights are loaded once), warp = every (NT2/32)-th window row
   const int nc2 = o2b - o2a;
-  for (int e = threadIdx.x; e < IR * TO2; e += NT2) {
-    const int r = e / TO2, c2 = e - r * TO2;
-    double acc = 0.0;
-    if (c2 < nc2) {
-      const int o2 = o2a + c2;
-      const int st = __ldg(start + o2);
-      const int kn = min(W, nin - st);
-      const double* wr = w + (size_t)o2 * W;
-      const double* xr = xin + r * ICP + (st - i2a);
-      for (int k = 0; k < kn; ++k) acc = fma(__ldg(wr + k), xr[k], acc);
+  {
+    static_assert(TO2 == 32, "one lane per output column");
+    const int c2 = threadIdx.x & 31;
+    const bool on = c2 < nc2;
+    const int o2 = on ? o2a + c2 : o2a;
+    const int st = __ldg(start + o2);
+    const int kn = min(W, nin - st);
+    double wv[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) wv[k] = (on && k < kn) ? __ldg(w + (size_t)o2 * W + k) : 0.0;
+    const double* xc = xin + (st - i2a);
+    for (int r = threadIdx.x >> 5; r < IR; r += NT2 / 32) {
+      const double* xr = xc + r * ICP;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        if (k < kn) acc = fma(wv[k], xr[k], acc);
+      tmp[r * TO2 + c2] = acc;
     }
-    tmp[r * TO2 + c2] = acc;
   }
   __syncthreads();
   // axis 1: out[o1][o2] = sum_k T[o1][k] tmp[st(o1) - i1a + k][c2]
@@ -141,7 +156,12 @@ __global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ i
     const double* wr = w + (size_t)o1 * W;
     const double* tr = tmp + (st - i1a) * TO2 + c2;
     double acc = 0.0;
-    for (int k = 0; k < kn; ++k) acc = fma(__ldg(wr + k), tr[k * TO2], acc);
+    double wv[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) wv[k] = __ldg(wr + k);
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+      if (k < kn) acc = fma(wv[k], tr[k * TO2], acc);
     dst[(size_t)o1 * nout + o2a + c2] = old[u] + acc;   // old = 0 unless accumulating
   }
 }
@@ -150,9 +170,24 @@ __global__ void __launch_bounds__(NT2) k_transfer2d(const double* __restrict__ i
 static void transfer2d(Handle& h, const double* in, double* out, long long slabs, int nin, int nout, const int* start,
                        const double* w, int W, int win1, int win2, bool acc, cudaStream_t s) {
   const size_t smem = sizeof(double) * ((size_t)win1 * (win2 | 1) + (size_t)win1 * TO2);
-  ensure_smem_attr((const void*)k_transfer2d, smem);
   const dim3 grid((nout + TO2 - 1) / TO2, (nout + TO1 - 1) / TO1, (unsigned)slabs);
-  k_transfer2d<<<grid, NT2, smem, s>>>(in, out, nin, nout, start, w, W, acc ? 1 : 0);
+#define IGACD_T2D(WW)                                                                       \
+  case WW:                                                                                  \
+    ensure_smem_attr((const void*)k_transfer2d<WW>, smem);                                  \
+    k_transfer2d<WW><<<grid, NT2, smem, s>>>(in, out, nin, nout, start, w, acc ? 1 : 0);   \
+    break
+  switch (W) {
+    IGACD_T2D(1);
+    IGACD_T2D(2);
+    IGACD_T2D(3);
+    IGACD_T2D(4);
+    IGACD_T2D(5);
+    IGACD_T2D(6);
+    IGACD_T2D(7);
+    IGACD_T2D(8);
+    default: throw Error{IGACD_E_ARG, "transfer row width out of range"};
+  }
+#undef IGACD_T2D
   IGACD_LAUNCH_CHECK();
   count_launch(h);
 }

@@ -9,9 +9,13 @@
   (calls only oracle/; the oracle runs take minutes).
 
 Tolerances (reading R9): apply-type results 1e-12 of max|oracle|; V-cycle and
-preconditioner actions max(1e-12, 10 u kappa(A_coarsest)) -- V b is not damped by a following
-step, so the exact coarse solve's rounding (dense inverse here, Cholesky in the oracle) carries
-kappa of the coarsest level; solves: iterations +-1, requested residual, ||dx||/||x|| <= 1e-8.
+preconditioner actions max(1e-12, 10 u kappa(A_coarsest)): the coarsest-level correction
+A_c^{-1} r_c is conditioned by kappa(A_c) with respect to the rounding of its own right-hand
+side r_c (restriction, residual), which no two implementations share, so u kappa(A_c) is the
+resolution of V b itself, however exactly A_c is solved (measured in round 2: one step of
+iterative refinement of the coarse solve on both sides left 1.2e-11 at kappa = 1.4e5); solves:
+iterations +-1 -- for the 530-iteration full-size solve, twice the spread the oracle's own
+count shows under rounding-level perturbations -- requested residual, ||dx||/||x|| <= 1e-8.
 """
 import os
 
