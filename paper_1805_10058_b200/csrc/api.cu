@@ -121,7 +121,7 @@ static void destroy_handle(Handle* h) {
   cudaFree(h->partial);
   cudaFree(h->scal);
   if (h->hscal) cudaFreeHost(h->hscal);
-  for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar, h->zbuf}) cudaFree(v);
+  for (double* v : {h->pr, h->pz, h->pp, h->pq, h->px, h->pb, h->aw, h->ar, h->zbuf, h->zbuf1}) cudaFree(v);
   for (double* v : {h->gm_v, h->gm_z, h->gm_partial, h->gm_dev}) cudaFree(v);
   if (h->gm_host) cudaFreeHost(h->gm_host);
   if (h->gA) cudaGraphExecDestroy(h->gA);
@@ -337,11 +337,15 @@ static Handle* create_impl(int dim, int p, int n, const double* mass, const doub
     IGACD_CUDA(cudaMalloc(&h->scratch0, sizeof(double) * scratch));
     IGACD_CUDA(cudaMalloc(&h->scratch1, sizeof(double) * scratch));
     size_t np = 1;
-    if (dim == 3) {   // z workspace of the split operator (the levels that take it): 3 * dim * m^3 doubles
-      size_t zmax = 0;
-      for (const Level& L : h->lv)
-        if (L.m % 2 == 1 || !apply3d_marching_pays(L.m) || split3d_forced()) zmax = std::max(zmax, L.nscal);
+    if (dim == 3) {   // z workspaces of the split operator (the levels that take it): 3 nc m^3 doubles
+      size_t zmax = 0, zmax1 = 0;
+      for (const Level& L : h->lv) {
+        const bool small = !apply3d_marching_pays(L.m) || split3d_forced();
+        if (small || L.m % 2 == 1) zmax = std::max(zmax, L.nscal);
+        if (small) zmax1 = std::max(zmax1, L.nscal);
+      }
       if (zmax) IGACD_CUDA(cudaMalloc(&h->zbuf, sizeof(double) * 3 * (size_t)dim * zmax));
+      if (zmax1) IGACD_CUDA(cudaMalloc(&h->zbuf1, sizeof(double) * 3 * zmax1));
     }
     for (size_t l = 0; l < ns.size(); ++l) {
       np = std::max(np, (size_t)operator_ctas(*h, (int)l));

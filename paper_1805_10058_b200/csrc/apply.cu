@@ -257,14 +257,16 @@ static Grid grid_for(const Handle& h, int level, int nc) {
 // the vector system's odd-m levels and the levels too small for marching to pay take the split
 // slab + column kernels (split3d.cu)
 static bool use_split(const Handle& h, int nc, int m) {
-  return h.dim == 3 && nc == 3 && h.zbuf && (m % 2 == 1 || !apply3d_marching_pays(m) || split3d_forced());
+  if (h.dim != 3 || !(nc == 3 ? h.zbuf : h.zbuf1)) return false;
+  if (split3d_forced() || !apply3d_marching_pays(m)) return true;
+  return nc == 3 && m % 2 == 1;   // the cp.async marching kernel measured slower than the split form here
 }
 
 int operator_ctas_sys(const Handle& h, int level, int nc) {
   const int m = h.lv[level].m;
   if (h.dim == 3) {   // upper bound over the paths a launch may take
     int n = apply3d_ctas(h.p, nc, m);
-    if (nc == 3) n = std::max(n, split3d_ctas(m));
+    n = std::max(n, split3d_ctas(m));
     return n;
   }
   Grid g = grid_for(h, level, nc);
@@ -296,7 +298,7 @@ int launch_operator(Handle& h, int sy, int level, const double* x, double* out, 
   int nct = operator_ctas_sys(h, level, S.nc);
   if (dot != DOT_NONE && (size_t)nct > h.partial_len) throw Error{IGACD_E_ARG, "partial buffer too small"};
   if (use_split(h, S.nc, op.m)) {
-    launch_split3d(h.p, op, epi, mode, dot, x, out, h.zbuf, s);
+    launch_split3d(h.p, S.nc, op, epi, mode, dot, x, out, S.nc == 3 ? h.zbuf : h.zbuf1, s);
     nct = split3d_ctas(op.m);
     count_launch(h);   // slab + column kernels
   } else if (h.dim == 3) {

@@ -135,6 +135,7 @@ struct Handle {
   double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr, *px = nullptr, *pb = nullptr;
   double *aw = nullptr, *ar = nullptr;   // aux preconditioner work (level-0 vector size)
   double* zbuf = nullptr;                // 3D split operator (split3d.cu): 3 nc per-point combinations
+  double* zbuf1 = nullptr;               // the same for the scalar system (it may run concurrently)
   // FGMRES workspace (allocated on first use): Arnoldi basis V [restart+1][N], Z [restart][N]
   int gm_restart = 0;
   double* gm_v = nullptr;
@@ -202,7 +203,7 @@ bool apply3d_marching_pays(int m);
 // ---- split3d.cu: the vector system's slab + column kernels (z through zbuf), odd-m levels ---
 bool split3d_forced();   // IGACD_SPLIT=1: on every level (comparison)
 int split3d_ctas(int m);
-void launch_split3d(int p, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+void launch_split3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
                     double* Z, cudaStream_t s);
 
 // ---- transfer.cu --------------------------------------------------------------------

@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(32) k_band_solve_tma(const __grid_constant__ C
                                                        double* __restrict__ data, int m,
                                                        long long inner, int tiles_per_outer, long long ntiles,
                                                        long long lines, const double* __restrict__ fac, int kc,
-                                                       int mode, double omega, double* __restrict__ xacc, int dbgsel) {
+                                                       int mode, double omega, double* __restrict__ xacc) {
   extern __shared__ __align__(128) double sht[];
   double* sh = sht;
   constexpr int WP = (W + 1) / 2 * 2;
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(32) k_band_solve_tma(const __grid_constant__ C
     const long long o = CONTIG ? 0 : g / tiles_per_outer;
     const long long i0 = CONTIG ? g * 32 : (g - o * tiles_per_outer) * 32;   // first line (CONTIG) / inner index
     const int nl = (int)min(32LL, (CONTIG ? lines : inner) - i0);
-    if (lane == 0 && dbgsel != 2) {
+    if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(ls_u32(mbar)),
                    "r"((unsigned)(nelem * 8))
@@ -426,7 +426,6 @@ __global__ void __launch_bounds__(32) k_band_solve_tma(const __grid_constant__ C
             "l"((unsigned long long)&tsrc), "r"((int)i0), "r"(-W), "r"((int)o), "r"(ls_u32(mbar))
             : "memory");
     }
-    if (dbgsel != 2) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -437,8 +436,6 @@ __global__ void __launch_bounds__(32) k_band_solve_tma(const __grid_constant__ C
         "r"(phase)
         : "memory");
     phase ^= 1u;
-    }
-    if (dbgsel == 1) { __syncwarp(); continue; }
     if (lane < nl) {
       band_sweep_s<W, true>(line, TP, gF, gI, m, kc);
       if (mode == 0) band_sweep_s<W, false>(line, TP, gB, gI, m, kc);
@@ -542,7 +539,6 @@ static bool try_tma(double* data, long long outer, int m, long long inner, const
   const int rows = m + 2 * (contig ? WP : W);
   const double* dst = mode == 0 ? data : xacc;
   const int mask = band_tma_mask();
-  static const int dbgsel = [] { const char* e = getenv("IGACD_BAND_DBG"); return (e && *e) ? atoi(e) : 0; }();
   if (!(mask & (contig ? 2 : 1)) || (mode == 1 && !(mask & 4))) return false;
   if (m % 2 || rows > 256 || outer * inner < 64LL * num_sms()) return false;
   if (((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return false;
@@ -558,10 +554,10 @@ static bool try_tma(double* data, long long outer, int m, long long inner, const
   const CUtensorMap td = contig ? ts : line_map(dst, outer, m, inner, W, false, false);   // output box: rows 0..m-1
   if (contig)
     k_band_solve_tma<W, true><<<blocks, 32, smem, s>>>(ts, td, data, m, inner, tpo, ntiles, lines, F.fac, F.kc, mode, omega,
-                                                       xacc, dbgsel);
+                                                       xacc);
   else
     k_band_solve_tma<W, false><<<blocks, 32, smem, s>>>(ts, td, data, m, inner, tpo, ntiles, lines, F.fac, F.kc, mode, omega,
-                                                        xacc, dbgsel);
+                                                        xacc);
   return true;
 }
 

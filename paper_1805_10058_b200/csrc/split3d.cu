@@ -1,6 +1,8 @@
-// R2 in 3D, vector system (nc = 3): the round-1 split form of the operator.  It serves the
-// levels with odd m (rows not 16-byte aligned, so no TMA: ws3d.cu does not apply), where it
-// measured faster than the cp.async marching kernel of apply3d.cu:
+// R2 in 3D: the round-1 split form of the operator.  It serves the levels on which the
+// marching kernel of apply3d.cu does not pay: too few output slabs per CTA for its 2p warm-up
+// slabs (every level but the largest ones), and the vector system's odd-m levels (no TMA)
+// (DESIGN.md "Kernels").  Each system has its own z workspace (the additive preconditioner runs
+// the two systems concurrently):
 //   k_slab3d  one CTA per (in-slab tile, slab): directions 1 and 2 from shared memory and the
 //             9 per-point combinations z_{i,F0} written to global memory (zbuf);
 //   k_col3d   one thread per (direction-1, direction-2) column: the direction-0 band scatter into
@@ -334,10 +336,15 @@ void launch_split_t(const OpParams& op, const Epi& ep, int mode, int dot, const 
 }
 
 template <int P>
-void launch_split_p(const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y, double* Z,
-                    cudaStream_t s) {
-  if (t3_split(op.m) == 27) launch_split_t<P, 3, 27>(op, ep, mode, dot, x, y, Z, s);
-  else launch_split_t<P, 3, 32>(op, ep, mode, dot, x, y, Z, s);
+void launch_split_p(int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+                    double* Z, cudaStream_t s) {
+  if (nc == 1) {
+    if (t3_split(op.m) == 27) launch_split_t<P, 1, 27>(op, ep, mode, dot, x, y, Z, s);
+    else launch_split_t<P, 1, 32>(op, ep, mode, dot, x, y, Z, s);
+  } else {
+    if (t3_split(op.m) == 27) launch_split_t<P, 3, 27>(op, ep, mode, dot, x, y, Z, s);
+    else launch_split_t<P, 3, 32>(op, ep, mode, dot, x, y, Z, s);
+  }
 }
 
 }  // namespace
@@ -355,15 +362,15 @@ int split3d_ctas(int m) {
   return ((m * m + 255) / 256) * ((m + chunk - 1) / chunk);
 }
 
-void launch_split3d(int p, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
+void launch_split3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
                     double* Z, cudaStream_t s) {
   switch (p) {
-    case 1: launch_split_p<1>(op, ep, mode, dot, x, y, Z, s); break;
-    case 2: launch_split_p<2>(op, ep, mode, dot, x, y, Z, s); break;
-    case 3: launch_split_p<3>(op, ep, mode, dot, x, y, Z, s); break;
-    case 4: launch_split_p<4>(op, ep, mode, dot, x, y, Z, s); break;
-    case 5: launch_split_p<5>(op, ep, mode, dot, x, y, Z, s); break;
-    case 6: launch_split_p<6>(op, ep, mode, dot, x, y, Z, s); break;
+    case 1: launch_split_p<1>(nc, op, ep, mode, dot, x, y, Z, s); break;
+    case 2: launch_split_p<2>(nc, op, ep, mode, dot, x, y, Z, s); break;
+    case 3: launch_split_p<3>(nc, op, ep, mode, dot, x, y, Z, s); break;
+    case 4: launch_split_p<4>(nc, op, ep, mode, dot, x, y, Z, s); break;
+    case 5: launch_split_p<5>(nc, op, ep, mode, dot, x, y, Z, s); break;
+    case 6: launch_split_p<6>(nc, op, ep, mode, dot, x, y, Z, s); break;
     default: throw Error{IGACD_E_ARG, "degree out of range"};
   }
 }
