@@ -302,7 +302,7 @@ int launch_operator(Handle& h, int sy, int level, const double* x, double* out, 
     nct = split3d_ctas(op.m);
     count_launch(h);   // slab + column kernels
   } else if (h.dim == 3) {
-    nct = launch_apply3d(h.p, S.nc, op, epi, mode, dot, x, out, s);
+    nct = launch_apply3d(h.p, S.nc, op, epi, mode, dot, x, out, s, h.slot_share);
   } else {
     switch (h.p) {
       case 1: dispatch2d<1>(S.nc, g, op, epi, mode, dot, x, out, s); break;

@@ -610,7 +610,7 @@ struct M3Plan {
 };
 
 template <int P, int NC, int T1, int T2, int RH, bool TMA>
-static M3Plan plan_m3(int m) {
+static M3Plan plan_m3(int m, int slot_share = 100) {
   using Sh = M3<P, NC, T1, T2, RH>;
   auto kern = k_march3d<P, NC, T1, T2, RH, TMA>;
   ensure_smem_attr((const void*)kern, Sh::SMEM);
@@ -618,15 +618,15 @@ static M3Plan plan_m3(int m) {
   M3Plan pl;
   pl.ntx = (m + T2 - 1) / T2;
   pl.nty = (m + T1 - 1) / T1;
-  pl.ctas = march_ctas(occ * num_sms(), pl.ntx * pl.nty * m);
+  pl.ctas = march_ctas(std::max(1, occ * num_sms() * slot_share / 100), pl.ntx * pl.nty * m);
   return pl;
 }
 
 template <int P, int NC, int T1, int T2, int RH, bool TMA>
 static int launch_m3(const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
-                     cudaStream_t s) {
+                     cudaStream_t s, int slot_share) {
   using Sh = M3<P, NC, T1, T2, RH>;
-  const M3Plan pl = plan_m3<P, NC, T1, T2, RH, TMA>(op.m);
+  const M3Plan pl = plan_m3<P, NC, T1, T2, RH, TMA>(op.m, slot_share);
   CUtensorMap map;
   if constexpr (TMA) map = slab_map(x, op.m, NC, Sh::XP, Sh::HR);
   else std::memset(&map, 0, sizeof(map));
@@ -664,15 +664,15 @@ static bool tma_enabled() {
 // Returns the CTAs of the persistent grid = partial sums written when a DotMode is requested.
 template <int P, int NC>
 static int dispatch_m3(const OpParams* op, int m, const Epi* ep, int mode, int dot, const double* x, double* y,
-                       cudaStream_t s) {
+                       cudaStream_t s, int slot_share) {
   // TMA needs 16-byte aligned global rows (m even) and base address
   const bool tma = tma_enabled() && m % 2 == 0 && (!x || ((uintptr_t)x & 15) == 0);
   const int v = tile_variant(m, NC);
 #define IGACD_M3_CASE(T1, T2, RH)                                                                            \
   do {                                                                                                       \
     if (!op) return std::max(plan_m3<P, NC, T1, T2, RH, true>(m).ctas, plan_m3<P, NC, T1, T2, RH, false>(m).ctas); \
-    return tma ? launch_m3<P, NC, T1, T2, RH, true>(*op, *ep, mode, dot, x, y, s)                            \
-               : launch_m3<P, NC, T1, T2, RH, false>(*op, *ep, mode, dot, x, y, s);                          \
+    return tma ? launch_m3<P, NC, T1, T2, RH, true>(*op, *ep, mode, dot, x, y, s, slot_share)                \
+               : launch_m3<P, NC, T1, T2, RH, false>(*op, *ep, mode, dot, x, y, s, slot_share);              \
   } while (0)
   if (v == 0) IGACD_M3_CASE(9, 27, 9);
   IGACD_M3_CASE(8, 32, 4);
@@ -680,9 +680,11 @@ static int dispatch_m3(const OpParams* op, int m, const Epi* ep, int mode, int d
 }
 
 static int dispatch_p(int p, int nc, const OpParams* op, int m, const Epi* ep, int mode, int dot, const double* x,
-                      double* y, cudaStream_t s) {
-#define IGACD_M3_P(PP) \
-  case PP: return nc == 1 ? dispatch_m3<PP, 1>(op, m, ep, mode, dot, x, y, s) : dispatch_m3<PP, 3>(op, m, ep, mode, dot, x, y, s)
+                      double* y, cudaStream_t s, int slot_share = 100) {
+#define IGACD_M3_P(PP)                                                                        \
+  case PP:                                                                                    \
+    return nc == 1 ? dispatch_m3<PP, 1>(op, m, ep, mode, dot, x, y, s, slot_share)            \
+                   : dispatch_m3<PP, 3>(op, m, ep, mode, dot, x, y, s, slot_share)
   switch (p) {
 #ifdef IGACD_DEV_P
     IGACD_M3_P(IGACD_DEV_P);
@@ -700,8 +702,8 @@ static int dispatch_p(int p, int nc, const OpParams* op, int m, const Epi* ep, i
 }
 
 int launch_apply3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
-                   cudaStream_t s) {
-  return dispatch_p(p, nc, &op, op.m, &ep, mode, dot, x, y, s);
+                   cudaStream_t s, int slot_share) {
+  return dispatch_p(p, nc, &op, op.m, &ep, mode, dot, x, y, s, slot_share);
 }
 
 // The marching kernel pays 2p warm-up slabs per segment, so it needs enough output slabs per

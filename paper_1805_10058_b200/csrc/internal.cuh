@@ -136,6 +136,10 @@ struct Handle {
   double *aw = nullptr, *ar = nullptr;   // aux preconditioner work (level-0 vector size)
   double* zbuf = nullptr;                // 3D split operator (split3d.cu): 3 nc per-point combinations
   double* zbuf1 = nullptr;               // the same for the scalar system (it may run concurrently)
+  // share (percent) of the resident CTA slots a persistent kernel may take: 100 except inside the
+  // scalar branch of the additive preconditioner, whose low-priority persistent kernels would
+  // otherwise fill every SM and hold up the vector branch (a running CTA is never preempted)
+  int slot_share = 100;
   // FGMRES workspace (allocated on first use): Arnoldi basis V [restart+1][N], Z [restart][N]
   int gm_restart = 0;
   double* gm_v = nullptr;
@@ -195,7 +199,7 @@ int operator_ctas_sys(const Handle& h, int level, int nc);
 // y = epilogue(A x) in 3D (one persistent fused kernel per apply); returns the CTAs launched
 // (= partial sums written when a DotMode is requested); apply3d_ctas: upper bound for a level
 int launch_apply3d(int p, int nc, const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
-                   cudaStream_t s);
+                   cudaStream_t s, int slot_share = 100);
 int apply3d_ctas(int p, int nc, int m);
 bool apply3d_marching_pays(int m);
 

@@ -533,7 +533,7 @@ static int band_tma_mask() {
 
 template <int W>
 static bool try_tma(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode, double omega,
-                    double* xacc, const double* src, cudaStream_t s) {
+                    double* xacc, const double* src, cudaStream_t s, int slot_share) {
   const bool contig = inner == 1;
   const int WP = (W + 1) / 2 * 2;
   const int rows = m + 2 * (contig ? WP : W);
@@ -549,7 +549,8 @@ static bool try_tma(double* data, long long outer, int m, long long inner, const
   const void* kern = contig ? (const void*)k_band_solve_tma<W, true> : (const void*)k_band_solve_tma<W, false>;
   ensure_smem_attr(kern, smem);
   const int occ = max_active_blocks(kern, 32, smem);
-  const unsigned blocks = (unsigned)std::min<long long>(ntiles, (long long)occ * num_sms());
+  const unsigned blocks =
+      (unsigned)std::min<long long>(ntiles, std::max<long long>(1, (long long)occ * num_sms() * slot_share / 100));
   const CUtensorMap ts = line_map(src, contig ? lines : outer, m, inner, W, contig);
   const CUtensorMap td = contig ? ts : line_map(dst, outer, m, inner, W, false, false);   // output box: rows 0..m-1
   if (contig)
@@ -663,7 +664,7 @@ static int band_warps() {   // IGACD_BAND_WARPS: warps per CTA of the tiled line
 
 template <int W>
 static void launch_w(double* data, long long outer, int m, long long inner, const BandFactor& F, int mode,
-                     double omega, double* xacc, const double* src, cudaStream_t s) {
+                     double omega, double* xacc, const double* src, cudaStream_t s, int slot_share) {
   // double-buffered 32-line tiles (2 warps) when they fit, else the widest single-buffered tile
   if (band_nbuf() == 2 && try_tiled<W, 2, 32, 2>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
   // few long lines (2D: 2m per axis): 8-line tiles, so that more SMs run a recurrence
@@ -673,7 +674,7 @@ static void launch_w(double* data, long long outer, int m, long long inner, cons
   if (outer * inner < 64LL * num_sms() && try_tiled<W, 1, 8, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s))
     return;
   // many short lines (3D): TMA-staged 32-line tiles
-  if (try_tma<W>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
+  if (try_tma<W>(data, outer, m, inner, F, mode, omega, xacc, src, s, slot_share)) return;
   // one warp per CTA packs 5 tiles per SM for m = 162 (2 warps per CTA: 4)
   if (band_warps() == 1 && try_tiled<W, 1, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
   if (try_tiled<W, 2, 32, 1>(data, outer, m, inner, F, mode, omega, xacc, src, s)) return;
@@ -772,13 +773,13 @@ void launch_band_solve(Handle& h, int nc, int level, int axis, const BandFactor&
   for (int a = 0; a < axis; ++a) outer *= m;
   for (int a = axis + 1; a < h.dim; ++a) inner *= m;
   switch (F.w) {
-    case 0: launch_w<0>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
-    case 1: launch_w<1>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
-    case 2: launch_w<2>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
-    case 3: launch_w<3>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
-    case 4: launch_w<4>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
-    case 5: launch_w<5>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
-    case 6: launch_w<6>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s); break;
+    case 0: launch_w<0>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s, h.slot_share); break;
+    case 1: launch_w<1>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s, h.slot_share); break;
+    case 2: launch_w<2>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s, h.slot_share); break;
+    case 3: launch_w<3>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s, h.slot_share); break;
+    case 4: launch_w<4>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s, h.slot_share); break;
+    case 5: launch_w<5>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s, h.slot_share); break;
+    case 6: launch_w<6>(data, outer, (int)m, inner, F, mode, omega, xacc, src, s, h.slot_share); break;
     default: throw Error{IGACD_E_ARG, "band width out of range"};
   }
   IGACD_LAUNCH_CHECK();
