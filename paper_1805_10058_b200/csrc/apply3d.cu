@@ -5,11 +5,10 @@
 // The Galerkin matrix is sum_P C_P (x) F0_P (x) F1_P (x) F2_P with 1D factors M, A, S
 // (eq:matr_Amu3D PAPER.md:515-543; the L_A form of reading R1 has the same Kronecker
 // patterns, internal.cuh Coef).  The (direction 1, direction 2) plane is cut into T1 x T2
-// tiles; a work unit is (tile, output slab along direction 0), units are numbered tile-major,
-// and CTA b of the persistent grid owns the contiguous unit range [b U / G, (b+1) U / G): it
-// marches the slabs of a tile ("segment"), and a range that crosses a tile boundary starts a
-// new segment.  Every CTA therefore has the same number of output slabs (+-1); the price is
-// the 2p warm-up slabs at the start of each segment.  Per slab s of a segment:
+// tiles; a work unit is (tile, output slab along direction 0).  The host lays the units on a
+// line, weighted by the measured cost of their tile class, and cuts it into G pieces of equal
+// cost (m3_schedule); CTA b of the persistent grid marches the slabs of its piece tile by tile
+// ("segments"; each one pays 2p warm-up slabs).  Per slab s of a segment:
 //   * the slab tile with its p-halo, all components, arrives in shared memory by TMA
 //     (cp.async.bulk.tensor, out-of-domain elements zero-filled by the tensor map) into one of
 //     two buffers, each completing on its own mbarrier; levels whose row pitch is not 16-byte
@@ -34,7 +33,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <cstdio>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "internal.cuh"
@@ -80,6 +81,8 @@ __device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, int
       : "memory");
 }
 
+constexpr int M3_KSEG = 6;   // most segments of one CTA (host schedule); .w of the first = how many
+
 // ---- shape ------------------------------------------------------------------------------------
 template <int P, int NC, int T1, int T2, int RH>
 struct M3 {
@@ -113,7 +116,7 @@ struct M3 {
 template <int P, int NC, int T1, int T2, int RH, bool TMA>
 __global__ void __launch_bounds__(M3<P, NC, T1, T2, RH>::NT, M3<P, NC, T1, T2, RH>::MINB)
     k_march3d(const __grid_constant__ CUtensorMap tmx, const OpParams op, const Epi ep, int mode, int dot,
-              const double* __restrict__ x, double* __restrict__ y, int ntx, int nty, int zc, int zr,
+              const double* __restrict__ x, double* __restrict__ y, int ntx, const int4* __restrict__ segs,
               long long* __restrict__ dbg) {
   using Sh = M3<P, NC, T1, T2, RH>;
   constexpr int NT = Sh::NT, NP = Sh::NP, R = Sh::R, HC = Sh::HC, XP = Sh::XP, XS = Sh::XS, XB = Sh::XB;
@@ -159,53 +162,25 @@ __global__ void __launch_bounds__(M3<P, NC, T1, T2, RH>::NT, M3<P, NC, T1, T2, R
 
   double dsum = 0.0;
   unsigned nld = 0;   // slab tiles requested so far (uniform): tile n lands in x buffer n & 1
-  // ---- this CTA's unit range: units are (tile, output slab), tile-major; a unit costs 16, plus zc in
-  // a tile with boundary-zone columns (per-lane band rows in pass B) and zr in one with
-  // boundary-zone rows (band rows in pass A); every CTA gets the same cost
-  // (all threads compute the same numbers; the loops are over tile rows / columns only)
-  auto has_zone = [&](int t0, int tw) { return t0 < op.zoneL || min(t0 + tw, m) > op.zoneR; };
-  auto unit_cost = [&](int ty, int tx) { return 16 + (has_zone(tx * T2, T2) ? zc : 0) + (has_zone(ty * T1, T1) ? zr : 0); };
-  auto row_cost = [&](int ty) {   // cost of one row of tiles (ntx tiles, m units each)
-    long long c = 0;
-    for (int tx = 0; tx < ntx; ++tx) c += (long long)m * unit_cost(ty, tx);
-    return c;
-  };
-  long long ctot = 0;
-  for (int ty = 0; ty < nty; ++ty) ctot += row_cost(ty);
-  auto unit_of = [&](long long c) -> int {   // the unit at cumulative cost c
-    for (int ty = 0; ty < nty; ++ty) {
-      const long long rc = row_cost(ty);
-      if (c < rc) {
-        for (int tx = 0; tx < ntx; ++tx) {
-          const long long w = unit_cost(ty, tx);
-          if (c < w * m) return (ty * ntx + tx) * m + (int)(c / w);
-          c -= w * m;
-        }
-      }
-      c -= rc;
-    }
-    return ntx * nty * m;
-  };
-  int u = unit_of(ctot * blockIdx.x / gridDim.x);
-  const int u1 = unit_of(ctot * (blockIdx.x + 1) / gridDim.x);
-  if (dbg && tid == 0) {   // IGACD_A3_DBG: per-CTA record (SM, start, end, unit range)
+  // ---- this CTA's segments: (tile, first output slab, one past the last), built on the host
+  // (m3_schedule below): contiguous pieces of the cost-weighted unit order
+  const int nseg = segs[blockIdx.x * M3_KSEG].w;
+  if (dbg && tid == 0) {   // IGACD_A3_DBG: per-CTA record (SM, start, end, first segment)
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     dbg[blockIdx.x * 5 + 0] = smid;
     dbg[blockIdx.x * 5 + 1] = t0;
-    dbg[blockIdx.x * 5 + 3] = u;
-    dbg[blockIdx.x * 5 + 4] = u1;
+    dbg[blockIdx.x * 5 + 3] = nseg;
+    dbg[blockIdx.x * 5 + 4] = segs[blockIdx.x * M3_KSEG].x;
   }
 
 #pragma unroll 1
-  while (u < u1) {
+  for (int sg = 0; sg < nseg; ++sg) {
     // ---- segment: output slabs [c0, c1) of one tile ------------------------------------------
-    const int tile = u / m;
-    const int c0 = u - tile * m;
-    const int c1 = min(m, c0 + (u1 - u));
-    u += c1 - c0;
+    const int4 sd = segs[blockIdx.x * M3_KSEG + sg];
+    const int tile = sd.x, c0 = sd.y, c1 = sd.z;
     const int ty = tile / ntx, tx = tile - ty * ntx;
     const int r0 = ty * T1, q0 = tx * T2;
     const int tr = real ? tid / T2 : 0, tc = real ? tid % T2 : 0;   // lanes along direction 2
@@ -607,10 +582,93 @@ static int march_ctas(int slots, int units) {
 
 struct M3Plan {
   int ctas, ntx, nty;
+  const int4* segs;
 };
 
+// The schedule of one launch configuration: units are (tile, output slab); a unit costs 16, plus
+// zc in a tile with boundary-zone columns (per-lane band rows in pass B) and zr in one with
+// boundary-zone rows (band rows in pass A) -- the measured per-unit times of the four tile
+// classes (IGACD_A3_DBG timeline).  The units are laid on a line and cut into G pieces of equal
+// cost; a piece that crosses a run boundary becomes several segments (2p warm-up slabs each).
+//   order 0: tile-major, one run per tile (fewest segments);
+//   order 1 (default, nch = 2): chunk-major -- the slab range is cut into nch chunks and the tiles
+//            of a chunk follow each other column by column, so CTAs marching neighbouring tiles
+//            are closer in time and more of the tile halos hit the L2, at the price of more
+//            segments.  Measured (config 4, DRAM bytes per apply / time): order 0 354 MB / 0.305 ms;
+//            nch = 1 332 MB / 0.308; nch = 2 279 MB / 0.309; nch = 3 307 MB / 0.328 ms.
+static const int4* m3_schedule(int m, int zoneL, int zoneR, int t1, int t2, int G) {
+  static const int zc = std::max(0, env_int("IGACD_A3_ZC", 6)), zr = std::max(0, env_int("IGACD_A3_ZR", 12));
+  static const int order = env_int("IGACD_A3_ORDER", 1), nch = std::max(1, env_int("IGACD_A3_NCH", 2));
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int, int, int>, int4*> cache;
+  int dev = 0;
+  IGACD_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, m, zoneL, zoneR, t1, t2, G);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int ntx = (m + t2 - 1) / t2, nty = (m + t1 - 1) / t1;
+  auto has_zone = [&](int t0, int tw) { return t0 < zoneL || std::min(t0 + tw, m) > zoneR; };
+  struct Run { int tile, s0, s1, w; };
+  std::vector<Run> runs;
+  auto cost = [&](int ty, int tx) { return 16 + (has_zone(tx * t2, t2) ? zc : 0) + (has_zone(ty * t1, t1) ? zr : 0); };
+  if (order == 0) {
+    for (int ty = 0; ty < nty; ++ty)
+      for (int tx = 0; tx < ntx; ++tx) runs.push_back({ty * ntx + tx, 0, m, cost(ty, tx)});
+  } else {
+    const int lc = (m + nch - 1) / nch;
+    for (int c = 0; c * lc < m; ++c)
+      for (int tx = 0; tx < ntx; ++tx)
+        for (int ty = 0; ty < nty; ++ty) runs.push_back({ty * ntx + tx, c * lc, std::min(m, (c + 1) * lc), cost(ty, tx)});
+  }
+  long long ctot = 0;
+  for (const Run& r : runs) ctot += (long long)(r.s1 - r.s0) * r.w;
+  // position (run, slab) of cumulative cost c
+  auto locate = [&](long long c, size_t* ri, int* sl) {
+    for (size_t i = 0; i < runs.size(); ++i) {
+      const long long rc = (long long)(runs[i].s1 - runs[i].s0) * runs[i].w;
+      if (c < rc) {
+        *ri = i;
+        *sl = runs[i].s0 + (int)(c / runs[i].w);
+        return;
+      }
+      c -= rc;
+    }
+    *ri = runs.size();
+    *sl = 0;
+  };
+  std::vector<int4> h((size_t)G * M3_KSEG, make_int4(0, 0, 0, 0));
+  for (int b = 0; b < G; ++b) {
+    size_t r0, r1;
+    int a0, a1;
+    locate(ctot * b / G, &r0, &a0);
+    locate(ctot * (b + 1) / G, &r1, &a1);
+    int n = 0;
+    for (size_t r = r0; r < runs.size() && (r < r1 || (r == r1 && a1 > runs[r].s0)); ++r) {
+      const int c0 = r == r0 ? a0 : runs[r].s0;
+      const int c1 = r == r1 ? a1 : runs[r].s1;
+      if (c1 <= c0) continue;
+      if (n == M3_KSEG) throw Error{IGACD_E_ARG, "3D operator schedule: too many segments per CTA"};
+      h[(size_t)b * M3_KSEG + n] = make_int4(runs[r].tile, c0, c1, 0);
+      ++n;
+    }
+    h[(size_t)b * M3_KSEG].w = n;
+  }
+  // a schedule first needed while this thread captures a graph (the PCG graphs are captured
+  // after one eager iteration, so normally never): allocation and copy are legal in relaxed mode
+  cudaStreamCaptureMode cm = cudaStreamCaptureModeRelaxed;
+  IGACD_CUDA(cudaThreadExchangeStreamCaptureMode(&cm));
+  int4* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(int4) * h.size());
+  if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), sizeof(int4) * h.size(), cudaMemcpyHostToDevice);
+  cudaThreadExchangeStreamCaptureMode(&cm);
+  IGACD_CUDA(e);
+  cache[key] = d;
+  return d;
+}
+
 template <int P, int NC, int T1, int T2, int RH, bool TMA>
-static M3Plan plan_m3(int m, int slot_share = 100) {
+static M3Plan plan_m3(const OpParams* op, int m, int slot_share = 100) {
   using Sh = M3<P, NC, T1, T2, RH>;
   auto kern = k_march3d<P, NC, T1, T2, RH, TMA>;
   ensure_smem_attr((const void*)kern, Sh::SMEM);
@@ -619,6 +677,7 @@ static M3Plan plan_m3(int m, int slot_share = 100) {
   pl.ntx = (m + T2 - 1) / T2;
   pl.nty = (m + T1 - 1) / T1;
   pl.ctas = march_ctas(std::max(1, occ * num_sms() * slot_share / 100), pl.ntx * pl.nty * m);
+  pl.segs = op ? m3_schedule(m, op->zoneL, op->zoneR, T1, T2, pl.ctas) : nullptr;
   return pl;
 }
 
@@ -626,17 +685,14 @@ template <int P, int NC, int T1, int T2, int RH, bool TMA>
 static int launch_m3(const OpParams& op, const Epi& ep, int mode, int dot, const double* x, double* y,
                      cudaStream_t s, int slot_share) {
   using Sh = M3<P, NC, T1, T2, RH>;
-  const M3Plan pl = plan_m3<P, NC, T1, T2, RH, TMA>(op.m, slot_share);
+  const M3Plan pl = plan_m3<P, NC, T1, T2, RH, TMA>(&op, op.m, slot_share);
   CUtensorMap map;
   if constexpr (TMA) map = slab_map(x, op.m, NC, Sh::XP, Sh::HR);
   else std::memset(&map, 0, sizeof(map));
-  // extra cost of a unit (16) in a tile with boundary-zone columns / rows (measured per-CTA timelines)
-  static const int zc = std::max(0, env_int("IGACD_A3_ZC", 6)), zr = std::max(0, env_int("IGACD_A3_ZR", 12));
   static const int dbg_on = env_int("IGACD_A3_DBG", 0);               // per-CTA timeline on stderr (measurement)
   long long* dbg = nullptr;
   if (dbg_on && NC == dbg_on) IGACD_CUDA(cudaMalloc(&dbg, sizeof(long long) * 5 * pl.ctas));
-  k_march3d<P, NC, T1, T2, RH, TMA><<<pl.ctas, Sh::NT, Sh::SMEM, s>>>(map, op, ep, mode, dot, x, y, pl.ntx, pl.nty, zc, zr,
-                                                                     dbg);
+  k_march3d<P, NC, T1, T2, RH, TMA><<<pl.ctas, Sh::NT, Sh::SMEM, s>>>(map, op, ep, mode, dot, x, y, pl.ntx, pl.segs, dbg);
   if (dbg) {
     std::vector<long long> hb(5 * pl.ctas);
     IGACD_CUDA(cudaStreamSynchronize(s));
@@ -645,10 +701,10 @@ static int launch_m3(const OpParams& op, const Epi& ep, int mode, int dot, const
     long long t0 = hb[1];
     for (int b = 0; b < pl.ctas; ++b) t0 = std::min(t0, hb[b * 5 + 1]);
     for (int b = 0; b < pl.ctas; ++b) {
-      const int u0 = (int)hb[b * 5 + 3], u1 = (int)hb[b * 5 + 4];
-      fprintf(stderr, "A3DBG m %d cta %d sm %lld start_us %.1f dur_us %.1f units %d tile0 %d (ty %d tx %d) tile1 %d slab0 %d\n",
-              op.m, b, hb[b * 5], (hb[b * 5 + 1] - t0) * 1e-3, (hb[b * 5 + 2] - hb[b * 5 + 1]) * 1e-3, u1 - u0,
-              u0 / op.m, u0 / op.m / pl.ntx, u0 / op.m % pl.ntx, (u1 - 1) / op.m, u0 % op.m);
+      const int tile = (int)hb[b * 5 + 4];
+      fprintf(stderr, "A3DBG m %d cta %d sm %lld start_us %.1f dur_us %.1f segments %lld first tile %d (ty %d tx %d)\n",
+              op.m, b, hb[b * 5], (hb[b * 5 + 1] - t0) * 1e-3, (hb[b * 5 + 2] - hb[b * 5 + 1]) * 1e-3, hb[b * 5 + 3],
+              tile, tile / pl.ntx, tile % pl.ntx);
     }
   }
   return pl.ctas;
@@ -670,7 +726,9 @@ static int dispatch_m3(const OpParams* op, int m, const Epi* ep, int mode, int d
   const int v = tile_variant(m, NC);
 #define IGACD_M3_CASE(T1, T2, RH)                                                                            \
   do {                                                                                                       \
-    if (!op) return std::max(plan_m3<P, NC, T1, T2, RH, true>(m).ctas, plan_m3<P, NC, T1, T2, RH, false>(m).ctas); \
+    if (!op)                                                                                                 \
+      return std::max(plan_m3<P, NC, T1, T2, RH, true>(nullptr, m).ctas,                                     \
+                      plan_m3<P, NC, T1, T2, RH, false>(nullptr, m).ctas);                                   \
     return tma ? launch_m3<P, NC, T1, T2, RH, true>(*op, *ep, mode, dot, x, y, s, slot_share)                \
                : launch_m3<P, NC, T1, T2, RH, false>(*op, *ep, mode, dot, x, y, s, slot_share);              \
   } while (0)
