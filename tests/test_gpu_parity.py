@@ -476,8 +476,10 @@ def test_graph_replay_is_bit_identical_to_eager_launches():
                                   Case(2, 5, 60, levels=2)], ids=repr)
 def test_tsolve_matches_oracle(case):
     """Line solves alone: x = T^{-1} b (I_d (x) T(m_{p-1}) (x) ..) vs the oracle's sparse LU.
-    Cases span 2D narrow line tiles (8/4 lines), full 32-line tiles with ragged tails, and the
-    3D slab kernel (directions 1 and 2 in one shared-memory pass)."""
+    These sizes run the narrow line tiles (8/4 lines per warp, ragged tails) and the 3D slab
+    kernel (directions 1 and 2 in one shared-memory pass); the 32-line tiles (TMA-staged and
+    cp.async) need >= 64 lines per SM and are covered at full configuration size by
+    test_gpu_parity_expected.py::test_tsolve_full_config_size_32_line_tiles."""
     h = case.handle()
     try:
         # T_n^p (PAPER.md:1204-1210) does not depend on the operator, so the oracle hierarchy is
