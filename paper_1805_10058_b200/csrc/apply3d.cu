@@ -334,11 +334,14 @@ __global__ void __launch_bounds__(M3<P, NC, T1, T2, RH>::NT, M3<P, NC, T1, T2, R
         passA(xs + ((nb + k + 1) & 1u) * XB, us + ((k + 1) & 1) * UB);
       }
       double fin[NC];   // final value of slab s - P
+      // z stays zero when the slab has no data (s >= m: the ring drains) or the thread no point:
+      // pass C then only shifts the ring, through the same instructions (a third code path that
+      // shifted by moves cost register copies at the merge)
+      double zM[NC], zS[NC], zA[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) zM[i] = zS[i] = zA[i] = 0.0;
       if (s < m && active) {
         // ---- pass B: direction 2 and the pattern combinations
-        double zM[NC], zS[NC], zA[NC];
-#pragma unroll
-        for (int i = 0; i < NC; ++i) zM[i] = zS[i] = zA[i] = 0.0;
         const double* ub = us + (k & 1) * UB + bo;
         if (!wzb) {
 #pragma unroll
@@ -423,6 +426,8 @@ __global__ void __launch_bounds__(M3<P, NC, T1, T2, RH>::NT, M3<P, NC, T1, T2, R
               zM[i] = fma(C.AA[2][i][j], vAA[j], zM[i]);
             }
         }
+      }
+      {
         // ---- pass C: scatter along direction 0 into the ring (rows t = s-P+r) and shift it in the
         // same instructions: ring slot r-1 <- slot r + F[t][s] z(s); slot 0 + F[s-P][s] z(s) is the
         // final value of slab s-P.  When all rows are Toeplitz rows, F[t][s] = T[s-t] is a register
@@ -446,7 +451,7 @@ __global__ void __launch_bounds__(M3<P, NC, T1, T2, RH>::NT, M3<P, NC, T1, T2, R
           for (int r = 0; r < R; ++r) {
             const int t = s - P + r;
             const bool in = t >= 0 && t < m;
-            const int tcl = in ? t : s;                    // clamped row: the address is always in range
+            const int tcl = in ? t : min(s, m - 1);        // clamped row: the address is always in range
             const int kk = tcl * R + (s - tcl) + P;        // F[t][s]
             const double sel = in ? 1.0 : 0.0;
             const double wM = sel * __ldg(op.bM + kk), wS = sel * __ldg(op.bS + kk), wA = sel * __ldg(op.bA + kk);
@@ -460,14 +465,6 @@ __global__ void __launch_bounds__(M3<P, NC, T1, T2, RH>::NT, M3<P, NC, T1, T2, R
         }
 #pragma unroll
         for (int i = 0; i < NC; ++i) acc[i][R - 1] = 0.0;
-      } else {   // no data in this slab (s >= m: the ring drains) or no point
-#pragma unroll
-        for (int i = 0; i < NC; ++i) {
-          fin[i] = acc[i][0];
-#pragma unroll
-          for (int r = 0; r < R - 1; ++r) acc[i][r] = acc[i][r + 1];
-          acc[i][R - 1] = 0.0;
-        }
       }
       // ---- epilogue of slab t = s - P
       {
