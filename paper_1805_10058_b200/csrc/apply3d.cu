@@ -103,14 +103,13 @@ struct M3 {
   static constexpr int UP = (T2 % 16 == 0) ? HC : HC + (((T2 - HC) % 16) + 16) % 16;
   static constexpr int US = T1 * UP;                    // one pass-A output array
   static constexpr int UB = 3 * NC * US;                // one u buffer: [F][j][T1][UP]
-  static constexpr int NSEG = T1 / RH;                  // pass-A row segments
+  static constexpr int NSEG = (T1 + RH - 1) / RH;       // pass-A row segments (the last may be shorter)
   static constexpr int NITEMS = NC * NSEG * HC;         // pass-A items (component, segment, column)
   static constexpr int IPT = (NITEMS + NT - 1) / NT;    // items per thread
   static constexpr int LPT = (NC * XS + NT - 1) / NT;   // cp.async path: copies per thread
   static constexpr int WZ = 3 * R * T2;                 // direction-2 band rows of the tile's columns
   static constexpr size_t SMEM = (size_t)(2 * XB + 2 * UB + WZ) * 8 + 16 + (NT / 32) * 8;
   static constexpr int MINB = NC == 3 ? 2 : 3;
-  static_assert(T1 % RH == 0, "row segments");
 };
 
 template <int P, int NC, int T1, int T2, int RH, bool TMA>
@@ -250,11 +249,13 @@ __global__ void __launch_bounds__(M3<P, NC, T1, T2, RH>::NT, M3<P, NC, T1, T2, R
           double* uo = ub + a_u[i];
           const int g0 = r0 + a_r[i];             // global row of the first output
           const bool zone_any = g0 < op.zoneL || g0 + RH > op.zoneR;
+          constexpr bool RAGGED = T1 % RH != 0;   // rows past the tile in the last segment
           double win[RH + 2 * P];
 #pragma unroll
-          for (int k = 0; k < RH + 2 * P; ++k) win[k] = col[k * XP];
+          for (int k = 0; k < RH + 2 * P; ++k) win[k] = (!RAGGED || a_r[i] + k < T1 + 2 * P) ? col[k * XP] : 0.0;
 #pragma unroll
           for (int r = 0; r < RH; ++r) {
+            if (RAGGED && a_r[i] + r >= T1) break;
             double vm, vs, va;
             const int g1 = g0 + r;
             if (zone_any && (g1 < op.zoneL || g1 >= op.zoneR)) {   // band row (uniform over the item's lanes)
@@ -558,13 +559,15 @@ static int env_int(const char* name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
-// tile variants: 0 = 9 x 27 (m = 162: 18 x 6 tiles, no padding), 1 = 8 x 32.  The vector system
-// takes the one with fewer padded thread slots; the scalar system measured faster on 8 x 32 rows
-// of full warps even with the padding (config 4: 0.144 vs 0.163 ms).
+// tile variants: 0 = 9 x 27 (m = 162: 18 x 6 tiles, no padding), 1 = 8 x 32: the one with fewer
+// padded thread slots.  Pass A splits the tile rows into segments so that there is about one
+// item (component, segment, halo column) per thread -- 9 x 27: rows 5 + 4 (vector), 3 x 3
+// (scalar); with one 9-row item per column only 105 of 243 threads had pass-A work and the
+// others waited at the barrier (config 4: 0.305 -> 0.272 ms, scalar 0.129 -> 0.117 ms).
 static int tile_variant(int m, int nc) {
   static const int force = env_int("IGACD_A3_TILE", -1);
+  (void)nc;
   if (force >= 0) return force;
-  if (nc == 1) return 1;
   auto padded = [&](int t1, int t2, int nt) {   // thread slots per slab
     return (double)((m + t1 - 1) / t1) * ((m + t2 - 1) / t2) * nt;
   };
@@ -721,16 +724,17 @@ static int dispatch_m3(const OpParams* op, int m, const Epi* ep, int mode, int d
   // TMA needs 16-byte aligned global rows (m even) and base address
   const bool tma = tma_enabled() && m % 2 == 0 && (!x || ((uintptr_t)x & 15) == 0);
   const int v = tile_variant(m, NC);
-#define IGACD_M3_CASE(T1, T2, RH)                                                                            \
+#define IGACD_M3_CASE(T1, T2, RH3, RH1)                                                                      \
   do {                                                                                                       \
+    constexpr int RH = NC == 3 ? RH3 : RH1;   /* pass-A rows per item: about one item per thread */          \
     if (!op)                                                                                                 \
       return std::max(plan_m3<P, NC, T1, T2, RH, true>(nullptr, m).ctas,                                     \
                       plan_m3<P, NC, T1, T2, RH, false>(nullptr, m).ctas);                                   \
     return tma ? launch_m3<P, NC, T1, T2, RH, true>(*op, *ep, mode, dot, x, y, s, slot_share)                \
                : launch_m3<P, NC, T1, T2, RH, false>(*op, *ep, mode, dot, x, y, s, slot_share);              \
   } while (0)
-  if (v == 0) IGACD_M3_CASE(9, 27, 9);
-  IGACD_M3_CASE(8, 32, 4);
+  if (v == 0) IGACD_M3_CASE(9, 27, 5, 3);
+  IGACD_M3_CASE(8, 32, 4, 2);
 #undef IGACD_M3_CASE
 }
 
